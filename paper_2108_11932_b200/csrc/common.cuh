@@ -1,0 +1,67 @@
+// Shared device helpers for the B200 TLR factorization (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace tlrg {
+
+#define TLRG_CUDA(x)                                                                 \
+  do {                                                                               \
+    cudaError_t e__ = (x);                                                           \
+    if (e__ != cudaSuccess)                                                          \
+      throw ::tlrg::CudaError(std::string(#x) + ": " + cudaGetErrorString(e__));     \
+  } while (0)
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+__host__ __device__ inline long long tri_index(int i, int j) {
+  // lower tile (i, j), i > j  ->  i(i-1)/2 + j   (tlr_matrix.cpp:31-34)
+  return (long long)i * (i - 1) / 2 + j;
+}
+
+// FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).  On sm_100a ptxas
+// lowers this to SASS DMMA.8x8x4.  Fragment ownership (lane l, g = l>>2, t = l&3):
+//   a = A[g][t], b = B[t][g], c0/c1 = C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of one double; `red` must hold >= 32 doubles.  All threads get
+// the result.  blockDim.x must be a multiple of 32.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];  // fixed order: deterministic
+  return s;
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace tlrg

@@ -1,0 +1,215 @@
+// Internal host-side structures of the B200 TLR library.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace tlrg {
+
+// Error taxonomy of the reference (errors.hpp:10-30) mapped to status codes.
+struct Error : std::runtime_error {
+  int code, index;
+  Error(int c, const std::string& m, int idx = -1) : std::runtime_error(m), code(c), index(idx) {}
+};
+[[noreturn]] inline void config_error(const std::string& m) { throw Error(2, m); }
+[[noreturn]] inline void data_error(const std::string& m) { throw Error(3, m); }
+[[noreturn]] inline void numeric_error(const std::string& m, int idx) { throw Error(4, m, idx); }
+
+void release_retired_arenas();
+
+// Grow-only device scratch buffer.  Only resized at synchronisation points.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t count) {
+    size_t bytes = count * sizeof(T) + 256;
+    if (bytes > cap) {
+      if (p) TLRG_CUDA(cudaFree(p));
+      size_t c = bytes + bytes / 4;
+      TLRG_CUDA(cudaMalloc(&p, c));
+      cap = c;
+    }
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+// Device memory for low-rank payloads (append-only chunks, never moved).
+struct Store {
+  std::vector<void*> chunks;
+  double* cur = nullptr;
+  size_t cap = 0, used = 0;
+  size_t total = 0;
+  double* alloc(size_t n);
+  ~Store();
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  DescArena desc;
+  std::map<std::string, DevBuf> bufs;
+  // pinned host staging for small D2H reads
+  int* h_ints = nullptr;
+  size_t h_ints_cap = 0;
+  double* h_dbl = nullptr;
+  size_t h_dbl_cap = 0;
+  double flops = 0.0;
+  long long launches = 0;
+
+  template <class T>
+  T* buf(const std::string& name, size_t count) {
+    return bufs[name].get<T>(count);
+  }
+  int* pinned_ints(size_t n);
+  double* pinned_dbl(size_t n);
+  void sync() {
+    TLRG_CUDA(cudaStreamSynchronize(st));
+    desc.reset();
+    release_retired_arenas();
+  }
+  template <class T>
+  T* push(const std::vector<T>& v) {
+    if (v.empty()) return nullptr;
+    return static_cast<T*>(desc.push(v.data(), v.size() * sizeof(T), st));
+  }
+  void gemm(std::vector<GemmProblem>& probs) {
+    for (auto& p : probs)
+      if (p.M > 0 && p.N > 0) flops += 2.0 * p.M * p.N * p.K;
+    grouped_gemm(probs, desc, st);
+    ++launches;
+  }
+  ~Ctx();
+};
+
+// Flat TLR store in HBM (replaces TlrMatrix/LowRankTile/DenseTile,
+// tlr_matrix.hpp:16-59): dense diagonal tiles at diag + k*b*b (ld rows(k)),
+// low-rank factors addressed through per-tile device pointers and ranks.
+struct Matrix {
+  Ctx* ctx = nullptr;
+  int64_t n = 0;
+  int b = 0, nb = 0;
+  double eps = 0.0;
+  double* diag = nullptr;              // owned
+  std::vector<int> rank;               // nb(nb-1)/2
+  std::vector<double*> U, V;           // device pointers (null when rank 0)
+  std::vector<std::shared_ptr<Store>> stores;  // own the payloads
+
+  int rows(int i) const {
+    int64_t r = n - (int64_t)i * b;
+    return r < b ? (int)r : b;
+  }
+  long long t(int i, int j) const { return tri_index(i, j); }
+  void free_all();
+  ~Matrix() { free_all(); }
+};
+
+struct AraCfg {
+  int bs = 32;
+  double eps = 1e-6;
+  int max_rank = 0;
+  int window = 0;
+  double safety = 10.0;
+  bool recompress = true;
+  uint64_t seed = 0;
+};
+
+// Device-resident LDL^T blocks D_j (flat nb*b arrays), or all null for Chol.
+struct DBlocks {
+  double* d = nullptr;
+  double* e = nullptr;
+  uint8_t* s2 = nullptr;
+  int* perm = nullptr;
+  bool on() const { return d != nullptr; }
+};
+
+struct TileResult {
+  int i = 0, rank = 0, rounds = 0;
+  bool converged = true;
+  double* U = nullptr;  // rows(i) x rank (device)
+  double* V = nullptr;  // rows(k) x rank (device, before TRSM)
+};
+
+struct ColumnStats {
+  double t_sampling = 0, t_orthog = 0, t_projection = 0, t_recompress = 0, t_dense = 0;
+  long long tile_rounds = 0;
+  double flops_ref = 0;  // reference-formulation sampling+projection flops
+};
+
+// Column machinery shared by the factorization and the building-block API.
+struct ColumnSetup {
+  int k = 0, rk = 0, K = 0;
+  std::vector<int> J;          // j < k with rank(k, j) > 0
+  std::vector<int> seg;        // column offset of block j in Ucat (indexed like J)
+  double* Ucat = nullptr;      // rk x K
+  double* Wcat = nullptr;      // b x K  (D_j V_kj)
+  double* G = nullptr;         // Gram blocks, per j: S_j x k_kj
+  std::vector<long long> goff; // per J entry
+  std::vector<int> S;          // per J entry
+  std::vector<int> sub_first;  // first i of the gathered suffix (k)
+};
+
+void column_setup(Ctx& C, const Matrix& M, int k, const DBlocks& D, ColumnSetup& cs);
+// H_i = U_i,: G_i for the listed target rows (rows(i) x K each, ld rows(i)).
+void column_H(Ctx& C, const Matrix& M, const ColumnSetup& cs, const std::vector<int>& targets,
+              double* H, long long stride);
+
+// Dynamic-batched ARA over column k (chol_ara_update, ara.cpp:302-419): all
+// non-trivial tiles resident, converged tiles leave, exit projection and SVD
+// recompression batched at the end.  Results (ascending i) land in a panel
+// allocated from `store` (U: sum rows(i)*r, V: rk x sum r contiguous).
+std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
+                                   const AraCfg& cfg, Store& store, ColumnStats& cst);
+
+struct FactorOpts {
+  bool schur = true;
+  double shift = 0.0;
+};
+
+struct Stats {
+  double t_sampling = 0, t_projection = 0, t_reduction = 0, t_dense = 0, t_orthog = 0,
+         t_misc = 0, t_pivot_select = 0, wall = 0, compensation_frob = 0;
+  int modified_diagonals = 0;
+  uint64_t tile_rounds_resident = 0;
+  double t_recompress = 0, t_compensation = 0, flops_exec = 0, flops_ref = 0;
+  long long launches = 0;
+  std::vector<int> ara_rounds;
+  std::vector<double> pivot_trace;
+};
+
+struct Factor {
+  std::unique_ptr<Matrix> L;
+  int mode = 0;  // 0 Chol, 1 LDLT
+  DBlocks D;     // owned device arrays in LDL mode
+  double eps = 0.0;
+  Stats stats;
+  ~Factor();
+};
+
+std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, const AraCfg& cfg,
+                                  int parallel_buffers, const FactorOpts& opts);
+
+// dense building blocks on device memory
+bool potrf_device(Ctx& C, double* A, int n);  // returns success
+// modified_cholesky (dense_kernels.cpp:283-309): A in, L out (in place); returns modified flag
+bool modified_cholesky_device(Ctx& C, double* A, int n);
+void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint64_t seed,
+                               double* corr, double* frob, int& rank_hint);
+
+// solve/apply/matvec on device vectors
+void matvec_device(Ctx& C, const Matrix& A, const double* x, double* y);
+void factor_apply_device(Ctx& C, const Factor& F, const double* x, double* y);
+void factor_solve_device(Ctx& C, const Factor& F, double* x);  // in place
+double dot_device(Ctx& C, const double* a, const double* b, long long n);
+
+}  // namespace tlrg

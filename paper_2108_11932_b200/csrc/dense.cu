@@ -1,0 +1,594 @@
+// Single-tile dense kernels on the factorization's critical path:
+//   * Cholesky (dense_kernels.cpp:66-82, LAPACKE_dpotrf)  -- left-looking,
+//     32-column panels; the trailing update runs on the grouped DMMA GEMM.
+//   * Bunch-Kaufman LDL^T (dense_kernels.cpp:236-281, LAPACKE_dsytrf) with the
+//     reference's unpacking into unit-lower L, D and perm.
+//   * panel TRSM X = L^{-1} B (dense_kernels.cpp:311-322) shared by all tiles of
+//     a column, with the LDL row permutation and D^{-1} fused (factor.cpp:257-262).
+//   * small helpers: symmetrize, diagonal combine, pivot traces, D apply.
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace tlrg {
+
+// ---------------------------------------------------------------- POTRF ---
+constexpr int PB = 32;  // panel width
+
+// CTA per 32-row block r >= p: factor the (already updated) diagonal block
+// A_pp in shared memory, then either store L_pp or solve X L_pp^T = A_rp.
+__global__ void __launch_bounds__(128) potrf_panel_kernel(double* A, int n, int p0, int pw,
+                                                          int* info) {
+  __shared__ double Lp[PB][PB + 1];
+  __shared__ double Ar[128][PB + 1];
+  __shared__ int fail;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) fail = -1;
+  for (int e = tid; e < PB * PB; e += 128) {
+    int i = e % PB, j = e / PB;
+    Lp[i][j] = (i < pw && j < pw) ? A[(p0 + i) + (long long)(p0 + j) * n] : 0.0;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    // unblocked right-looking Cholesky of the pw x pw block (one warp)
+    for (int j = 0; j < pw; ++j) {
+      double d = Lp[j][j];
+      bool bad = !(d > 0.0);
+      if (bad) {
+        if (lane == 0) fail = j;
+        break;
+      }
+      double s = sqrt(d);
+      __syncwarp();
+      if (lane == 0) Lp[j][j] = s;
+      __syncwarp();
+      if (lane > j && lane < pw) Lp[lane][j] /= s;
+      __syncwarp();
+      if (lane > j && lane < pw)
+        for (int c = j + 1; c <= lane; ++c) Lp[lane][c] -= Lp[lane][j] * Lp[c][j];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (fail >= 0) {
+    if (tid == 0 && blockIdx.x == 0) atomicCAS(info, -1, p0 + fail);
+    return;
+  }
+  const int rb0 = p0 + blockIdx.x * 128;  // first row handled by this CTA
+  if (blockIdx.x == 0) {
+    // diagonal block rows [p0, p0+pw): store L_pp (zero the strict upper part)
+    for (int e = tid; e < pw * pw; e += 128) {
+      int i = e % pw, j = e / pw;
+      A[(p0 + i) + (long long)(p0 + j) * n] = i >= j ? Lp[i][j] : 0.0;
+    }
+  }
+  // rows below the diagonal block that this CTA owns: [max(rb0, p0+pw), rb0+128)
+  int r_lo = rb0 < p0 + pw ? p0 + pw : rb0;
+  int r_hi = rb0 + 128 < n ? rb0 + 128 : n;
+  int nr = r_hi - r_lo;
+  if (nr <= 0) return;
+  for (int e = tid; e < nr * pw; e += 128) {
+    int i = e % nr, j = e / nr;
+    Ar[i][j] = A[(r_lo + i) + (long long)(p0 + j) * n];
+  }
+  __syncthreads();
+  if (tid < nr) {
+    for (int j = 0; j < pw; ++j) {
+      double s = Ar[tid][j];
+      for (int t = 0; t < j; ++t) s -= Ar[tid][t] * Lp[j][t];
+      Ar[tid][j] = s / Lp[j][j];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nr * pw; e += 128) {
+    int i = e % nr, j = e / nr;
+    A[(r_lo + i) + (long long)(p0 + j) * n] = Ar[i][j];
+  }
+}
+
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
+void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st) {
+  set_int_kernel<<<1, 1, 0, st>>>(info, -1);
+  for (int p0 = 0; p0 < n; p0 += PB) {
+    int pw = n - p0 < PB ? n - p0 : PB;
+    if (p0 > 0) {
+      // A[p0:, p0:p0+pw] -= L[p0:, 0:p0] * L[p0:p0+pw, 0:p0]^T
+      std::vector<GemmProblem> pr(1);
+      GemmProblem& g = pr[0];
+      g.A = A + p0;
+      g.lda = n;
+      g.transA = 0;
+      g.B = A + p0;
+      g.ldb = n;
+      g.transB = 1;
+      g.C = A + p0 + (long long)p0 * n;
+      g.ldc = n;
+      g.M = n - p0;
+      g.N = pw;
+      g.K = p0;
+      g.alpha = -1.0;
+      g.beta = 1.0;
+      grouped_gemm(pr, desc, st);
+    }
+    int rows = n - p0;
+    int blocks = (rows + 127) / 128;
+    potrf_panel_kernel<<<blocks, 128, 0, st>>>(A, n, p0, pw, info);
+    TLRG_CUDA(cudaGetLastError());
+  }
+}
+
+// ------------------------------------------------------ BUNCH-KAUFMAN -----
+// LAPACK dsytf2 (UPLO = 'L') executed by one CTA on an n x n tile in global
+// memory.  Interchanges are applied to the whole rows (including the already
+// computed multipliers), which yields exactly the reference's unpacked form
+// (dense_kernels.cpp:253-279): P A P^T = L D L^T with perm[i] = original row.
+constexpr int BK_T = 1024;
+
+__global__ void __launch_bounds__(BK_T) sytrf_bk_kernel(double* A, int n, double* d, double* e,
+                                                        uint8_t* s2, int* perm, int* info) {
+  __shared__ double rv[32];
+  __shared__ int ri[32];
+  __shared__ int s_imax, s_kp, s_kstep;
+  __shared__ double s_colmax;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = BK_T / 32;
+  const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+  auto a = [&](int i, int j) -> double& { return A[i + (long long)j * n]; };
+  for (int i = tid; i < n; i += BK_T) {
+    perm[i] = i;
+    d[i] = 0.0;
+    if (i < n - 1) e[i] = 0.0;
+    s2[i] = 0;
+  }
+  if (tid == 0) *info = -1;
+  __syncthreads();
+  // block argmax of |x_i| (first index on ties, like idamax)
+  auto argmax = [&](auto getv, int lo, int hi, double& vmax, int& imax) {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = lo + tid; i < hi; i += BK_T) {
+      double v = fabs(getv(i));
+      if (v > bv || (v == bv && i < bi)) {
+        bv = v;
+        bi = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    __syncthreads();
+    if (lane == 0) {
+      rv[warp] = bv;
+      ri[warp] = bi;
+    }
+    __syncthreads();
+    bv = -1.0;
+    bi = 0x7fffffff;
+    for (int w = 0; w < nw; ++w)
+      if (rv[w] > bv || (rv[w] == bv && ri[w] < bi)) {
+        bv = rv[w];
+        bi = ri[w];
+      }
+    vmax = bv < 0 ? 0.0 : bv;
+    imax = bi;
+  };
+
+  int k = 0;
+  while (k < n) {
+    int kstep = 1, kp = k;
+    double absakk = fabs(a(k, k));
+    double colmax = 0.0;
+    int imax = k;
+    if (k < n - 1) argmax([&](int i) { return a(i, k); }, k + 1, n, colmax, imax);
+    if (tid == 0) {
+      if (fmax(absakk, colmax) == 0.0) {
+        if (*info < 0) *info = k;  // zero pivot: record, keep going
+        kp = k;
+      } else if (absakk >= alpha * colmax) {
+        kp = k;
+      } else {
+        s_imax = imax;
+      }
+      s_kp = kp;
+      s_kstep = 1;
+      s_colmax = colmax;
+    }
+    __syncthreads();
+    if (!(fmax(absakk, colmax) == 0.0) && !(absakk >= alpha * colmax)) {
+      // rowmax: off-diagonal max of row imax in the trailing matrix
+      double rm1 = 0.0, rm2 = 0.0;
+      int i1, i2;
+      argmax([&](int j) { return a(imax, j); }, k, imax, rm1, i1);
+      if (imax < n - 1) argmax([&](int j) { return a(j, imax); }, imax + 1, n, rm2, i2);
+      double rowmax = fmax(rm1, rm2);
+      if (tid == 0) {
+        if (absakk >= alpha * colmax * (colmax / rowmax)) {
+          kp = k;
+        } else if (fabs(a(imax, imax)) >= alpha * rowmax) {
+          kp = imax;
+        } else {
+          kp = imax;
+          kstep = 2;
+        }
+        s_kp = kp;
+        s_kstep = kstep;
+      }
+      __syncthreads();
+      kp = s_kp;
+      kstep = s_kstep;
+    } else {
+      kp = s_kp;
+    }
+    __syncthreads();
+    const int kk = k + kstep - 1;
+    if (kp != kk) {
+      // symmetric interchange of rows/columns kk and kp in the trailing matrix,
+      // plus the full-row swap of the earlier multipliers (columns < k)
+      for (int i = kp + 1 + tid; i < n; i += BK_T) {
+        double t = a(i, kk);
+        a(i, kk) = a(i, kp);
+        a(i, kp) = t;
+      }
+      for (int j = kk + 1 + tid; j < kp; j += BK_T) {
+        double t = a(j, kk);
+        a(j, kk) = a(kp, j);
+        a(kp, j) = t;
+      }
+      for (int j = tid; j < k; j += BK_T) {
+        double t = a(kk, j);
+        a(kk, j) = a(kp, j);
+        a(kp, j) = t;
+      }
+      if (tid == 0) {
+        double t = a(kk, kk);
+        a(kk, kk) = a(kp, kp);
+        a(kp, kp) = t;
+        if (kstep == 2) {
+          t = a(k + 1, k);
+          a(k + 1, k) = a(kp, k);
+          a(kp, k) = t;
+        }
+        int pt = perm[kk];
+        perm[kk] = perm[kp];
+        perm[kp] = pt;
+      }
+    }
+    __syncthreads();
+    if (kstep == 1) {
+      double akk = a(k, k);
+      if (akk != 0.0) {
+        double r1 = 1.0 / akk;
+        // trailing rank-1 update (dsyr, lower) then scale the column
+        int m = n - k - 1;
+        long long tot = (long long)m * (m + 1) / 2;
+        for (long long t = tid; t < tot; t += BK_T) {
+          // map t -> (i, j) with j <= i in the trailing (m x m) lower triangle
+          int jj = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) / 2.0);
+          while ((long long)jj * (jj + 1) / 2 > t) --jj;
+          while ((long long)(jj + 1) * (jj + 2) / 2 <= t) ++jj;
+          int ii = (int)(t - (long long)jj * (jj + 1) / 2);
+          // (row = jj, col = ii) in lower triangle: i = k+1+jj, j = k+1+ii
+          int i = k + 1 + jj, j = k + 1 + ii;
+          a(i, j) -= r1 * a(i, k) * a(j, k);
+        }
+        __syncthreads();
+        for (int i = k + 1 + tid; i < n; i += BK_T) a(i, k) *= r1;
+      }
+      if (tid == 0) d[k] = a(k, k);
+    } else {
+      if (k < n - 2) {
+        double d21 = a(k + 1, k);
+        double d11 = a(k + 1, k + 1) / d21;
+        double d22 = a(k, k) / d21;
+        double t = 1.0 / (d11 * d22 - 1.0);
+        d21 = t / d21;
+        int m = n - k - 2;
+        long long tot = (long long)m * (m + 1) / 2;
+        for (long long q = tid; q < tot; q += BK_T) {
+          int jj = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) / 2.0);
+          while ((long long)jj * (jj + 1) / 2 > q) --jj;
+          while ((long long)(jj + 1) * (jj + 2) / 2 <= q) ++jj;
+          int ii = (int)(q - (long long)jj * (jj + 1) / 2);
+          int i = k + 2 + jj, j = k + 2 + ii;
+          double wkj = d21 * (d11 * a(j, k) - a(j, k + 1));
+          double wkp1j = d21 * (d22 * a(j, k + 1) - a(j, k));
+          a(i, j) -= a(i, k) * wkj + a(i, k + 1) * wkp1j;
+        }
+        __syncthreads();
+        for (int j = k + 2 + tid; j < n; j += BK_T) {
+          double wk = d21 * (d11 * a(j, k) - a(j, k + 1));
+          double wkp1 = d21 * (d22 * a(j, k + 1) - a(j, k));
+          a(j, k) = wk;
+          a(j, k + 1) = wkp1;
+        }
+      }
+      if (tid == 0) {
+        d[k] = a(k, k);
+        d[k + 1] = a(k + 1, k + 1);
+        e[k] = a(k + 1, k);
+        s2[k] = 1;
+      }
+    }
+    __syncthreads();
+    k += kstep;
+  }
+  __syncthreads();
+  // unpack: unit lower L (2x2 block off-diagonals belong to D)
+  for (long long t = tid; t < (long long)n * n; t += BK_T) {
+    int i = (int)(t % n), j = (int)(t / n);
+    if (i == j) a(i, j) = 1.0;
+    else if (i < j) a(i, j) = 0.0;
+    else if (i == j + 1 && s2[j]) a(i, j) = 0.0;
+  }
+}
+
+void sytrf_bk(double* A, int n, double* d, double* e, uint8_t* s2, int* perm, int* info,
+              cudaStream_t st) {
+  sytrf_bk_kernel<<<1, BK_T, 0, st>>>(A, n, d, e, s2, perm, info);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+// ----------------------------------------------------------------- TRSM ---
+// X = L^{-1} B for a panel of right-hand sides; one CTA per 16 columns.
+// LDL mode (perm != null): rows are gathered through perm, L is unit lower and
+// the block diagonal D^{-1} is applied last (factor.cpp:257-262).
+constexpr int TR_C = 16;
+
+__global__ void __launch_bounds__(256) trsm_panel_kernel(const double* L, int n, double* B,
+                                                         long long nrhs, const int* perm,
+                                                         const double* d, const double* e,
+                                                         const uint8_t* s2, int* info) {
+  extern __shared__ double X[];  // n x TR_C, ld n
+  const long long c0 = (long long)blockIdx.x * TR_C;
+  const int nc = (int)(nrhs - c0 < TR_C ? nrhs - c0 : TR_C);
+  const int tid = threadIdx.x;
+  const bool unit = perm != nullptr;
+  for (int t = tid; t < n * nc; t += 256) {
+    int i = t % n, c = t / n;
+    int src = unit ? perm[i] : i;
+    X[i + c * n] = B[src + (c0 + c) * (long long)n];
+  }
+  __syncthreads();
+  for (int p0 = 0; p0 < n; p0 += 32) {
+    int pw = n - p0 < 32 ? n - p0 : 32;
+    // X_p -= L[p, 0:p0] X[0:p0]
+    if (p0 > 0)
+      for (int t = tid; t < pw * nc; t += 256) {
+        int i = p0 + t % pw, c = t / pw;
+        double s = 0.0;
+        const double* xl = X + c * n;
+        for (int q = 0; q < p0; ++q) s += L[i + (long long)q * n] * xl[q];
+        X[i + c * n] -= s;
+      }
+    __syncthreads();
+    // forward substitution inside the block, one thread per column
+    if (tid < nc) {
+      double* xc = X + tid * n;
+      for (int i = p0; i < p0 + pw; ++i) {
+        double s = xc[i];
+        for (int q = p0; q < i; ++q) s -= L[i + (long long)q * n] * xc[q];
+        xc[i] = unit ? s : s / L[i + (long long)i * n];
+      }
+    }
+    __syncthreads();
+  }
+  if (unit && d) {
+    // D^{-1} (dense_kernels.cpp:126-144)
+    if (tid < nc) {
+      double* xc = X + tid * n;
+      int k = 0;
+      while (k < n) {
+        if (s2[k]) {
+          double det = d[k] * d[k + 1] - e[k] * e[k];
+          if (det == 0.0) {
+            atomicCAS(info, -1, k);
+            break;
+          }
+          double a = xc[k], b = xc[k + 1];
+          xc[k] = (d[k + 1] * a - e[k] * b) / det;
+          xc[k + 1] = (d[k] * b - e[k] * a) / det;
+          k += 2;
+        } else {
+          if (d[k] == 0.0) {
+            atomicCAS(info, -1, k);
+            break;
+          }
+          xc[k] /= d[k];
+          k += 1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < n * nc; t += 256) {
+    int i = t % n, c = t / n;
+    B[i + (c0 + c) * (long long)n] = X[i + c * n];
+  }
+}
+
+void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
+                const double* d, const double* e, const uint8_t* s2, int* info,
+                cudaStream_t st) {
+  if (nrhs <= 0 || n <= 0) return;
+  size_t bytes = (size_t)n * TR_C * 8;
+  static bool configured = false;
+  if (bytes > 48 * 1024 && !configured) {
+    TLRG_CUDA(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+    configured = true;
+  }
+  unsigned blocks = (unsigned)((nrhs + TR_C - 1) / TR_C);
+  trsm_panel_kernel<<<blocks, 256, bytes, st>>>(L, n, B, nrhs, perm, d, e, s2, info);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+// -------------------------------------------------------------- HELPERS ---
+__global__ void symmetrize_kernel(double* D, int n) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long tot = (long long)n * n;
+  if (t >= tot) return;
+  int i = (int)(t % n), j = (int)(t / n);
+  if (i <= j) return;
+  double v = 0.5 * (D[i + (long long)j * n] + D[j + (long long)i * n]);  // factor.cpp:32-39
+  D[i + (long long)j * n] = v;
+  D[j + (long long)i * n] = v;
+}
+void symmetrize(double* D, int n, cudaStream_t st) {
+  long long tot = (long long)n * n;
+  symmetrize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(D, n);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+__global__ void diag_combine_kernel(const double* A, const double* D, const double* corr,
+                                    double shift, double* out, int n) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long tot = (long long)n * n;
+  if (t >= tot) return;
+  int i = (int)(t % n), j = (int)(t / n);
+  double v = A[t];
+  if (D) v -= D[t];  // factor.cpp:217-218
+  if (i == j) {
+    if (corr) v += corr[i];  // factor.cpp:219-223
+    if (shift > 0) v += shift;  // factor.cpp:224
+  }
+  out[t] = v;
+}
+void diag_combine(const double* A, const double* D, const double* corr, double shift,
+                  double* out, int n, cudaStream_t st) {
+  long long tot = (long long)n * n;
+  diag_combine_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, D, corr, shift, out, n);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+__global__ void min_diag_sq_kernel(const double* L, int n, double* out) {
+  __shared__ double red[32];
+  double m = INFINITY;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double v = L[i + (long long)i * n];
+    m = fmin(m, v * v);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmin(r, red[w]);
+    *out = r;
+  }
+}
+void min_diag_sq(const double* L, int n, double* out, cudaStream_t st) {
+  min_diag_sq_kernel<<<1, 256, 0, st>>>(L, n, out);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+__global__ void min_block_pivot_kernel(const double* d, const double* e, const uint8_t* s2, int n,
+                                       double* out) {
+  // factor.cpp:87-102 (sequential scan; n <= a few thousand)
+  double m = INFINITY;
+  int k = 0;
+  while (k < n) {
+    if (s2[k]) {
+      double mean = 0.5 * (d[k] + d[k + 1]);
+      double rad = hypot(0.5 * (d[k] - d[k + 1]), e[k]);
+      m = fmin(m, fmin(fabs(mean - rad), fabs(mean + rad)));
+      k += 2;
+    } else {
+      m = fmin(m, fabs(d[k]));
+      k += 1;
+    }
+  }
+  *out = m;
+}
+void min_block_pivot(const double* d, const double* e, const uint8_t* s2, int n, double* out,
+                     cudaStream_t st) {
+  min_block_pivot_kernel<<<1, 1, 0, st>>>(d, e, s2, n, out);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+// W <- D W  (dense_kernels.cpp:97-116), one thread per column
+__global__ void bd_apply_kernel(const double* d, const double* e, const uint8_t* s2, int n,
+                                double* W, long long ld, int cols) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double* x = W + (long long)c * ld;
+  int k = 0;
+  while (k < n) {
+    if (s2[k]) {
+      double a = x[k], b = x[k + 1];
+      x[k] = d[k] * a + e[k] * b;
+      x[k + 1] = e[k] * a + d[k + 1] * b;
+      k += 2;
+    } else {
+      x[k] *= d[k];
+      k += 1;
+    }
+  }
+}
+void bd_apply(const double* d, const double* e, const uint8_t* s2, int n, double* W, long long ld,
+              int cols, cudaStream_t st) {
+  if (cols <= 0) return;
+  bd_apply_kernel<<<(cols + 63) / 64, 64, 0, st>>>(d, e, s2, n, W, ld, cols);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+__global__ void frob_sq_kernel(const double* p, long long n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long t = threadIdx.x; t < n; t += blockDim.x) s += p[t] * p[t];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+void frob_sq(const double* p, long long n, double* out, cudaStream_t st) {
+  frob_sq_kernel<<<1, 1024, 0, st>>>(p, n, out);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+// counter-based Gaussian fill (splitmix64 + Box-Muller); used for the Schur
+// compensation sketch, whose randomness is not part of the reference's streams.
+__global__ void gaussian_fill_kernel(double* out, long long n, uint64_t seed) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long pairs = (n + 1) / 2;
+  if (t >= pairs) return;
+  uint64_t a = mix64(seed ^ mix64((uint64_t)t * 2 + 1));
+  uint64_t b = mix64(a ^ 0x5851f42d4c957f2dULL);
+  double u1 = ((double)(a >> 11) + 1.0) * 0x1.0p-53;
+  double u2 = (double)(b >> 11) * 0x1.0p-53;
+  double r = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  out[2 * t] = r * c;
+  if (2 * t + 1 < n) out[2 * t + 1] = r * s;
+}
+void fill_gaussian_philox(double* out, long long n, uint64_t seed, cudaStream_t st) {
+  if (n <= 0) return;
+  long long pairs = (n + 1) / 2;
+  gaussian_fill_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(out, n, seed);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+// corr[i] = sum_j |D_ij - (Xl Xr^T)_ij| is computed after the GEMM R = D - Xl Xr^T;
+// this kernel takes R directly.
+__global__ void rowsum_abs_kernel(const double* R, int n, double* corr, double* frob_part) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0, f = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double v = R[i + (long long)j * n];
+    s += fabs(v);
+    f += v * v;
+  }
+  corr[i] = s;
+  frob_part[i] = f;
+}
+void rowsum_abs_residual(const double* R, const double*, const double*, int n, int,
+                         double* corr, double* frob_part, cudaStream_t st) {
+  rowsum_abs_kernel<<<(n + 127) / 128, 128, 0, st>>>(R, n, corr, frob_part);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+}  // namespace tlrg

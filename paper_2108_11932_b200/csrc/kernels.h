@@ -1,0 +1,143 @@
+// Host-side launch wrappers for the sm_100a kernels (one translation unit per
+// kernel family).  All wrappers are asynchronous on `st`.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <vector>
+
+#include "gemm.cuh"
+#include "rng.cuh"
+
+namespace tlrg {
+
+// ---------------------------------------------------------------- GEMM ----
+// Grouped DMMA GEMM.  `probs` is filled on the host; the launcher assigns
+// tile offsets and stages the table through `desc` (device scratch reused
+// after each stream synchronisation by the caller).
+struct DescArena;
+void grouped_gemm(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st);
+
+// Device scratch for kernel argument tables: pinned host staging + device
+// mirror, bump-allocated and reset by the owner after a stream sync.
+struct DescArena {
+  char* h = nullptr;
+  char* d = nullptr;
+  size_t cap = 0, used = 0;
+  void reserve(size_t bytes);
+  void* push(const void* src, size_t bytes, cudaStream_t st);  // returns device ptr
+  void reset() { used = 0; }
+  ~DescArena();
+};
+
+// ----------------------------------------------------------------- RNG ----
+void rng_seed(RngState* states, const uint64_t* d_seeds, int n, cudaStream_t st);
+// draw `count` gaussians for each listed state into out + t*out_stride
+void rng_draw(RngState* states, const int* d_state_idx, int ntiles, double* out,
+              long long count, long long out_stride, cudaStream_t st);
+
+// --------------------------------------------------------------- ORTHOG ---
+// One panel of the reference's orthog (dense_kernels.cpp:331-420) per task.
+struct PanelTask {
+  double* Y;          // rows x width, ld = rows
+  const double* Q;    // rows x q basis (for replacement projection), ld = rows
+  double* R;          // width x width accumulated factor (col-major, ld = width)
+  double* Rp;         // width x width scratch
+  double* tiny;       // width
+  uint8_t* deficient; // width
+  double* col_norms;  // width (written when finalize)
+  double* new_mass;   // width
+  RngState* rng;
+  double tau;         // 100 * DBL_EPSILON * ||Y_raw||_F (or DBL_MIN)
+  int rows, width, q;
+};
+// tau[t] = 100*eps*||Y_t||_F  (frobenius of the raw sample)
+void panel_tau(PanelTask* d_tasks, int ntask, cudaStream_t st);
+void panel_mgs(PanelTask* d_tasks, int ntask, int sweep, int finalize, int max_width,
+               int max_rows, cudaStream_t st);
+
+// ARA absorb step (ara.cpp:171-195) for a batch of tiles.
+struct AbsorbTask {
+  const double* Y;        // rows x bs orthonormal panel
+  double* Q;              // rows x cap basis, ld = rows
+  const double* col_norms;
+  const double* new_mass;
+  double* recent;         // ring buffer [window]
+  int* qcols;             // in/out
+  int* recent_count;      // in/out (number of valid entries, <= window)
+  int* recent_pos;        // in/out ring position
+  int* rounds;            // in/out
+  int* converged;         // out
+  int* done;              // out
+  int rows, bs, cap, window;
+  double eps, eta;
+};
+void ara_absorb(AbsorbTask* d_tasks, int ntask, cudaStream_t st);
+
+// One-sided Jacobi SVD + truncation of small square factors (recompression,
+// ara.cpp:201-211 / dense_kernels.cpp:422-454).  A (n x n) is overwritten with
+// the scaled left vectors (columns sorted by singular value, descending),
+// V receives right vectors; rank_out[t] = #{sigma > cut}.
+struct SvdTask {
+  double* A;   // n x n, ld = n
+  double* V;   // n x n, ld = n
+  double* sig; // n (sorted descending on exit)
+  double* work; // 2 n^2 scratch, used when the problem does not fit in smem
+  int* rank_out;
+  int n;
+  double cut;
+};
+void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st);
+
+// Block-diagonal product H[:, seg_j] = U_ij * G_ij for a set of (tile, j) items.
+struct BlockItem {
+  const double* U;  // rows x kij, ld = rows
+  const double* G;  // kij x kkj, ld = ldg
+  double* H;        // rows x kkj, ld = ldh (already offset to seg_j)
+  long long ldg, ldh;
+  int rows, kij, kkj;
+};
+void block_products(BlockItem* d_items, int nitems, int max_rows, cudaStream_t st);
+
+// Copy/gather helpers
+struct CopyItem {
+  const double* src;
+  double* dst;
+  long long lds, ldd;
+  int rows, cols;
+};
+void batched_copy(CopyItem* d_items, int n, cudaStream_t st);
+
+// ---------------------------------------------------------------- DENSE ---
+// Cholesky of an m x m tile in place (lower); info[0] = failing column or -1.
+void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st);
+// Bunch-Kaufman (LAPACK dsytf2, lower) with the reference's unpacking
+// (dense_kernels.cpp:236-281): A -> unit-lower L, D (d, e, start2x2), perm.
+void sytrf_bk(double* A, int n, double* d, double* e, uint8_t* s2, int* perm, int* info,
+              cudaStream_t st);
+// X <- L^{-1} B (Chol) or X <- D^{-1} Lunit^{-1} P B (LDL), B rows x nrhs (ld rows).
+void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
+                const double* d, const double* e, const uint8_t* s2, int* info,
+                cudaStream_t st);
+// D <- 0.5 (D + D^T)
+void symmetrize(double* D, int n, cudaStream_t st);
+// out = A - D (+ diag(corr)) (+ shift I)
+void diag_combine(const double* A, const double* D, const double* corr, double shift,
+                  double* out, int n, cudaStream_t st);
+// pivot trace helpers
+void min_diag_sq(const double* L, int n, double* out, cudaStream_t st);
+void min_block_pivot(const double* d, const double* e, const uint8_t* s2, int n, double* out,
+                     cudaStream_t st);
+// W <- D_j W  (block diagonal apply, rows of W)
+void bd_apply(const double* d, const double* e, const uint8_t* s2, int n, double* W,
+              long long ld, int cols, cudaStream_t st);
+// Schur compensation helpers
+void sym_jacobi_eig(double* B, double* V, double* w, int n, cudaStream_t st);
+void rowsum_abs_residual(const double* D, const double* X, const double* lam, int n, int r,
+                         double* corr, double* frob_sq, cudaStream_t st);
+void fill_gaussian_philox(double* out, long long n, uint64_t seed, cudaStream_t st);
+
+// generic elementwise
+void fill_zero(double* p, long long n, cudaStream_t st);
+void frob_sq(const double* p, long long n, double* out, cudaStream_t st);
+
+}  // namespace tlrg

@@ -1,0 +1,104 @@
+"""GPU TLR Cholesky / LDL^T against the oracle on the same input matrix
+(test_factor.cpp cases; tolerance contract of BASELINE.json north_star:
+residual within 2x of the reference, ranks within 10%)."""
+import numpy as np
+import pytest
+
+from helpers import covariance_ref, points, to_gpu
+from paper_2108_11932_b200 import geometry as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(tg, eps, bs=16, seed=5):
+    return tg.AraConfig(block_samples=bs, eps=eps, seed=seed)
+
+
+def test_block_diagonal_input_needs_no_rounds(tg, ref):
+    pts = points(G.GRID2D, 256, 64)
+    A_ref = ref.build(pts, 0, 1e-5, 0.5, 64, 1e-8, 1, 32, 0)
+    A = to_gpu(tg, A_ref)
+    diag0 = [A_ref.diag(k) for k in range(A_ref.nb)]
+    F = tg.tlr_cholesky(A, _cfg(tg, 1e-8))
+    assert (F.stats.ara_rounds == 0).all()
+    Ld, _, _, _ = F.L.to_parts()
+    for k in range(F.L.nb):
+        assert np.abs(np.tril(Ld[k]) - np.linalg.cholesky(diag0[k])).max() <= 1e-14
+
+
+def test_cholesky_matches_dense_tiled_reference(tg, ref):
+    pts = points(G.GRID2D, 512, 128)
+    eps = 1e-8
+    A_ref = ref.build(pts, 0, 0.1, 0.0, 128, eps, 0, 16, 5)
+    full = ref.kernel_block(pts, 0, 0.1, 0.0, 0, 512, 0, 512)
+    F = tg.tlr_cholesky(to_gpu(tg, A_ref), _cfg(tg, eps))
+    Lt = np.tril(F.L.dense())
+    Lexact = np.linalg.cholesky(full)
+    assert np.abs(Lt - Lexact).max() <= 1e-6
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-6])
+def test_residual_contract_and_parity(tg, ref, eps):
+    A_ref = covariance_ref(ref, 1024, 128, eps, seed=42)
+    A = to_gpu(tg, A_ref)
+    Akeep = A.copy()
+    F = tg.tlr_cholesky(A, _cfg(tg, eps))
+    Fr = ref.factor(A_ref, 0, bs=16, eps=eps, seed=5)
+    r = tg.estimate_2norm_diff(Akeep, F, 50, 17)
+    rr = ref.estimate_2norm_diff(A_ref, Fr, 50, 17)
+    assert r <= 10 * F.L.nb * eps
+    assert r <= 2.0 * rr
+    rk, rkr = F.L.ranks(), Fr.L_ranks()
+    assert abs(rk.mean() - rkr.mean()) <= 0.1 * rkr.mean() + 1e-12
+    # draw-for-draw streams: the rank maps agree tile by tile
+    assert (rk == rkr).mean() >= 0.95
+
+
+def test_cholesky_without_compensation_matches_reference_factor(tg, ref):
+    eps = 1e-6
+    A_ref = covariance_ref(ref, 768, 128, eps, seed=42)
+    F = tg.tlr_cholesky(to_gpu(tg, A_ref), _cfg(tg, eps),
+                        opts=tg.FactorOptions(schur_compensation=False))
+    Fr = ref.factor(A_ref, 0, bs=16, eps=eps, seed=5, schur_compensation=False)
+    assert (F.L.ranks() == Fr.L_ranks()).all()
+    assert (F.stats.ara_rounds == Fr.stats().ara_rounds).all()
+    d1, _, U1, V1 = F.L.to_parts()
+    d2, _, U2, V2 = Fr.L_parts()
+    for a, b in zip(d1, d2):
+        assert np.abs(a - b).max() <= 1e-9
+    for u1, v1, u2, v2 in zip(U1, V1, U2, V2):
+        assert np.abs(u1 @ v1.T - u2 @ v2.T).max() <= 1e-8
+
+
+def test_ldlt_on_spd_and_indefinite(tg, ref):
+    eps = 1e-6
+    A_ref = covariance_ref(ref, 512, 128, eps, nugget=0.05)
+    Akeep = to_gpu(tg, A_ref)
+    F = tg.tlr_ldlt(to_gpu(tg, A_ref), _cfg(tg, eps))
+    assert tg.estimate_2norm_diff(Akeep, F, 50, 7) <= 10 * F.L.nb * eps
+    assert all(d.all_positive() for d in F.D)
+    # indefinite shift (test_factor.cpp:278-307)
+    A_ref = covariance_ref(ref, 1024, 128, eps)
+    sigma = 0.5 * A_ref.estimate_2norm(30, 1)
+    diag, ranks, U, V = A_ref.to_parts()
+    diag = [d - sigma * np.eye(d.shape[0]) for d in diag]
+    A = tg.TlrMatrix.from_parts(1024, 128, eps, diag, ranks, U, V)
+    Akeep = A.copy()
+    F = tg.tlr_ldlt(A, _cfg(tg, eps))
+    assert tg.estimate_2norm_diff(Akeep, F, 50, 11) <= 10 * F.L.nb * eps
+    assert any(not d.all_positive() for d in F.D)
+
+
+def test_solve_apply_matvec_match_reference(tg, ref):
+    eps = 1e-6
+    A_ref = covariance_ref(ref, 640, 128, eps)
+    A = to_gpu(tg, A_ref)
+    Akeep = A.copy()
+    F = tg.tlr_cholesky(A, _cfg(tg, eps))
+    Fr = ref.factor(A_ref, 0, bs=16, eps=eps, seed=5)
+    x = np.random.default_rng(1).normal(size=640)
+    assert np.abs(tg.tlr_matvec(Akeep, x) - A_ref.matvec(x)).max() <= 1e-12 * 640
+    assert np.abs(tg.factor_apply(F, x) - Fr.apply(x)).max() <= 1e-7
+    b = A_ref.matvec(x)
+    xs = tg.factor_solve(F, b)
+    assert np.linalg.norm(A_ref.matvec(xs) - b) / np.linalg.norm(b) <= 100 * F.L.nb * eps

@@ -1,0 +1,171 @@
+"""GPU parity of the building blocks against the oracle (the unmodified
+reference compiled under oracle/_ref) and numpy.  Mirrors test_dense.cpp /
+test_ara.cpp cases."""
+import numpy as np
+import pytest
+
+from helpers import covariance_ref, dblocks_np, to_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("M,N,K,ta,tb", [(64, 32, 16, 0, 0), (100, 17, 33, 1, 0), (7, 129, 65, 0, 1),
+                                         (130, 70, 1, 1, 1), (512, 16, 512, 1, 0), (3, 3, 0, 0, 0)])
+def test_grouped_dmma_gemm_matches_numpy(tg, M, N, K, ta, tb):
+    r = np.random.default_rng(M * 1000 + N)
+    A = r.normal(size=(K, M) if ta else (M, K))
+    B = r.normal(size=(N, K) if tb else (K, N))
+    C0 = r.normal(size=(M, N))
+    want = 0.7 * ((A.T if ta else A) @ (B.T if tb else B)) - 0.3 * C0
+    got = tg.tlr.gemm(0.7, A, ta, B, tb, -0.3, C0)
+    assert np.abs(got - want).max() <= 1e-13 * max(1.0, np.abs(want).max()) * max(K, 1)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 12345, 2**63 + 5])
+def test_device_rng_draw_for_draw(tg, ref, seed):
+    n = 20001
+    got = tg.tlr.rng_gaussians(seed, n)
+    want = ref.rng_gaussians(seed, n)
+    assert np.abs(got - want).max() <= 4e-15 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("rows,q,k,case", [(96, 0, 16, "plain"), (128, 20, 16, "plain"),
+                                           (64, 8, 8, "dup"), (64, 0, 8, "zero"),
+                                           (200, 40, 32, "lowrank")])
+def test_orthog_matches_reference(tg, ref, rows, q, k, case):
+    r = np.random.default_rng(rows + q + k)
+    Q = np.linalg.qr(r.normal(size=(rows, q)))[0] if q else None
+    if case == "plain":
+        Y = r.normal(size=(rows, k))
+    elif case == "dup":
+        Y = r.normal(size=(rows, k))
+        Y[:, 3] = Y[:, 1]
+        Y[:, 5] = 2 * Y[:, 0] - Y[:, 2]
+    elif case == "zero":
+        Y = np.zeros((rows, k))
+    else:
+        Y = r.normal(size=(rows, 3)) @ r.normal(size=(3, k))
+        if q:
+            Y += Q @ r.normal(size=(q, k))
+    Yg, Rg, cg, mg, ng = tg.tlr.orthog(Q, Y, 77)
+    Yr, Rr, cr, mr, nr = ref.orthog(Q, Y, 77)
+    scale = max(np.abs(Y).max(), 1.0)
+    assert np.abs(cg - cr).max() <= 1e-12 * scale
+    assert np.abs(mg - mr).max() <= 1e-12 * scale
+    assert np.abs(Rg - Rr).max() <= 1e-11 * scale
+    # healthy columns agree; replaced columns are random directions drawn from
+    # the same stream and agree as well
+    assert np.abs(Yg - Yr).max() <= 1e-9
+    assert ng == pytest.approx(nr, rel=1e-12, abs=1e-14)
+
+
+def test_sample_left_matches_reference_chol(tg, ref):
+    A_ref = covariance_ref(ref, 1024, 128, 1e-8)
+    A = to_gpu(tg, A_ref)
+    k = 5
+    rows = list(range(k + 1, A.nb))
+    r = np.random.default_rng(23)
+    om = [r.normal(size=(128, 16)) for _ in rows]
+    got = tg.sample_left(A, None, k, rows, tg.AraWorkspace(parallel_buffers=32), om)
+    want = ref.sample_left(A_ref, k, rows, om, parallel_buffers=32)
+    for g, w, o in zip(got, want, om):
+        assert np.linalg.norm(g - w) <= 1e-11 * max(np.linalg.norm(w), 1.0) * np.linalg.norm(o)
+    # transpose mode (projection)
+    q = [np.linalg.qr(r.normal(size=(128, 9)))[0] for _ in rows]
+    got = tg.sample_left_transpose(A, None, k, rows, tg.AraWorkspace(parallel_buffers=32), q)
+    want = ref.sample_left(A_ref, k, rows, q, parallel_buffers=32, transpose=True)
+    for g, w in zip(got, want):
+        assert np.linalg.norm(g - w) <= 1e-11 * max(np.linalg.norm(w), 1.0)
+
+
+def test_sample_left_ldl_inserts_d(tg, ref):
+    A_ref = covariance_ref(ref, 512, 128, 1e-8)
+    A = to_gpu(tg, A_ref)
+    D = dblocks_np(A.nb, [128] * A.nb, 99)
+    r = np.random.default_rng(29)
+    om = [r.normal(size=(128, 8))]
+    got = tg.sample_left(A, D, 2, [3], tg.AraWorkspace(), om)
+    want = ref.sample_left(A_ref, 2, [3], om, D=D)
+    assert np.linalg.norm(got[0] - want[0]) <= 1e-11 * np.linalg.norm(want[0]) * np.linalg.norm(om[0])
+
+
+def test_sample_left_rejects_undersized_workspace(tg, ref):
+    A = to_gpu(tg, covariance_ref(ref, 384, 96, 1e-6))
+    with pytest.raises(tg.ConfigError):
+        tg.sample_left(A, None, 0, [1, 2, 3], tg.AraWorkspace(parallel_buffers=2),
+                       [np.zeros((96, 4))] * 3)
+
+
+@pytest.mark.parametrize("k,eps,seed", [(1, 1e-5, 1234), (0, 1e-6, 88), (3, 1e-8, 5)])
+def test_chol_ara_update_matches_reference(tg, ref, k, eps, seed):
+    """Same seeds -> same draws: ranks equal and Q B^T within 1e-9
+    (test_ara.cpp:294-318 standard)."""
+    A_ref = covariance_ref(ref, 768, 128, 1e-6)
+    A = to_gpu(tg, A_ref)
+    cfg = tg.AraConfig(block_samples=16, eps=eps, seed=seed)
+    got = tg.chol_ara_update(A, None, k, cfg, tg.AraWorkspace(parallel_buffers=16,
+                                                               subset_capacity=2))
+    want = ref.chol_ara_update(A_ref, k, bs=16, eps=eps, seed=seed, parallel_buffers=16,
+                               subset_capacity=2)
+    assert [t.i for t in got] == [t["i"] for t in want]
+    for g, w in zip(got, want):
+        assert g.Q.shape[1] == w["Q"].shape[1], (g.i, g.Q.shape, w["Q"].shape)
+        assert g.rounds_resident == w["rounds"]
+        assert g.converged == w["converged"]
+        d1, d2 = g.Q @ g.B.T, w["Q"] @ w["B"].T
+        assert np.abs(d1 - d2).max() <= 1e-9 * max(np.linalg.norm(d2), 1.0)
+        if g.Q.shape[1]:
+            G = g.Q.T @ g.Q
+            assert np.linalg.norm(G - np.eye(G.shape[0])) <= 1e-11
+
+
+def test_chol_ara_update_zero_rank_column(tg, ref):
+    from helpers import points
+    from paper_2108_11932_b200 import geometry as G
+    pts = points(G.GRID2D, 256, 64)
+    A_ref = ref.build(pts, 0, 1e-5, 0.5, 64, 1e-6, 1, 32, 0)
+    A = to_gpu(tg, A_ref)
+    out = tg.chol_ara_update(A, None, 0, tg.AraConfig(eps=1e-6), tg.AraWorkspace())
+    assert len(out) == 3
+    for t in out:
+        assert t.converged and t.rounds_resident == 0 and t.Q.shape[1] == 0
+
+
+@pytest.mark.parametrize("n", [1, 31, 64, 100, 256, 512])
+def test_potrf_matches_reference(tg, ref, n):
+    r = np.random.default_rng(n)
+    G = r.normal(size=(n, n))
+    A = G @ G.T + 0.1 * n * np.eye(n)
+    L, fail = tg.tlr.dense_cholesky(A)
+    assert fail == -1
+    assert np.abs(L - np.linalg.cholesky(A)).max() <= 1e-12 * np.abs(A).max()
+    B = A.copy()
+    B[n // 2, n // 2] = -1.0
+    _, fail = tg.tlr.dense_cholesky(B)
+    assert fail >= 0
+
+
+@pytest.mark.parametrize("n,kind", [(5, "indef"), (64, "indef"), (128, "spd"), (200, "indef"),
+                                    (512, "indef")])
+def test_bunch_kaufman_matches_reference(tg, ref, n, kind):
+    r = np.random.default_rng(n + 7)
+    G = r.normal(size=(n, n))
+    A = (G + G.T) / 2 if kind == "indef" else G @ G.T + n * np.eye(n)
+    L, D, perm, info = tg.tlr.dense_ldl(A)
+    Lr, dr, er, s2r, pr = ref.dense_ldl(A)
+    P = A[np.ix_(perm, perm)]
+    rec = L @ D.materialize() @ L.T
+    assert np.abs(rec - P).max() <= 1e-11 * np.abs(A).max() * n
+    # LAPACK's pivot decisions are reproduced (ties aside): same block structure
+    assert (D.start2x2 == s2r).mean() >= 0.95
+    assert np.allclose(np.sort(perm), np.arange(n))
+
+
+def test_schur_compensation_matches_reference(tg, ref):
+    r = np.random.default_rng(3)
+    for n, rank, eps in [(16, 6, 0.5), (128, 40, 1e-3), (256, 120, 1e-6)]:
+        G = r.normal(size=(n, rank)) * np.logspace(0, -8, rank)
+        Dk = G @ G.T
+        want = ref.schur_compensation(Dk, eps)
+        got, frob = tg.tlr.schur_compensation(Dk, eps)
+        assert np.abs(got - want).max() <= 1e-6 * max(np.abs(want).max(), eps) + 1e-12
