@@ -1,0 +1,315 @@
+// Batched adaptive randomized approximation (ARA) on the device.
+//
+// One call runs the reference's per-tile TileState machine (ara.cpp:155-195)
+// for a whole batch of tiles at once, with every tile resident (the GPU
+// replacement for the rank-sorted subset scheduler, ara.cpp:302-404: the
+// per-tile streams make results independent of the schedule, test_ara.cpp
+// "subset capacity changes scheduling only").  Per round:
+//   draw   : per-tile tlr::Rng gaussian blocks (exact mt19937_64 streams)
+//   sample : Y = E Omega  (operator callback -> grouped DMMA GEMMs)
+//   orthog : BGS2 against Q (grouped GEMMs) + per-tile MGS2 panel kernel
+//   absorb : keep filter, basis append, window convergence (device flags)
+// Converged tiles leave; one D2H of the flags per round drives compaction.
+// At the end all tiles are projected (B = E^T Q) and recompressed (orthog of B
+// + one-sided Jacobi SVD of R, cut at (1 - 1/eta) eps) in batches, and the
+// final factors are written into a contiguous panel.
+#include <algorithm>
+#include <numeric>
+
+#include "core.h"
+
+namespace tlrg {
+
+namespace {
+struct Timer {
+  cudaEvent_t a, b;
+  explicit Timer() {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  void start(cudaStream_t s) { cudaEventRecord(a, s); }
+  void stop(cudaStream_t s) { cudaEventRecord(b, s); }
+  double sec() {
+    float f = 0;
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&f, a, b);
+    return f * 1e-3;
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+}  // namespace
+
+void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,
+               const std::vector<int>& out_order, ColumnStats& cst, AraOut& out) {
+  const int T = (int)S.rows.size();
+  const int bs = cfg.bs, cols = S.cols;
+  const int window = cfg.window > 0 ? cfg.window : bs;
+  out.rank.assign(T, 0);
+  out.rounds.assign(T, 0);
+  out.conv.assign(T, 1);
+  out.U.assign(T, nullptr);
+  out.V.assign(T, nullptr);
+  if (T == 0) return;
+  int maxrows = 0, capmax = 0;
+  for (int s = 0; s < T; ++s) {
+    maxrows = std::max(maxrows, S.rows[s]);
+    capmax = std::max(capmax, S.cap[s]);
+  }
+  const long long Ystride = (long long)maxrows * bs, Qstride = (long long)maxrows * capmax;
+  double* Om = C.buf<double>("Om", (size_t)cols * bs * T);
+  double* Y = C.buf<double>("Y", (size_t)T * Ystride);
+  double* Q = C.buf<double>("Q", (size_t)T * Qstride);
+  double* Cdef = C.buf<double>("Cdef", (size_t)T * capmax * bs);
+  double* R = C.buf<double>("R", (size_t)T * bs * bs);
+  double* Rp = C.buf<double>("Rp", (size_t)T * 2 * bs * bs);
+  double* tiny = C.buf<double>("tiny", (size_t)T * bs);
+  uint8_t* defi = C.buf<uint8_t>("defi", (size_t)T * bs);
+  double* cn = C.buf<double>("cn", (size_t)T * bs);
+  double* nm = C.buf<double>("nm", (size_t)T * bs);
+  double* recent = C.buf<double>("recent", (size_t)T * window);
+  int* ints = C.buf<int>("ints", (size_t)T * 6);
+  int *qcols = ints, *rounds = ints + T, *conv = ints + 2 * T, *done = ints + 3 * T,
+      *rcount = ints + 4 * T, *rpos = ints + 5 * T;
+  RngState* rng = C.buf<RngState>("rng", (size_t)T);
+  TLRG_CUDA(cudaMemsetAsync(ints, 0, sizeof(int) * T * 6, C.st));
+  rng_seed(rng, C.push(S.seeds), T, C.st);
+  ++C.launches;
+
+  std::vector<int> q(T, 0);
+  std::vector<int> act(T);
+  std::iota(act.begin(), act.end(), 0);
+  int* h_flags = C.pinned_ints((size_t)2 * T);
+  Timer tm, to;
+  while (!act.empty()) {
+    const int Ta = (int)act.size();
+    tm.start(C.st);
+    rng_draw(rng, C.push(act), Ta, Om, (long long)cols * bs, (long long)cols * bs, C.st);
+    ++C.launches;
+    op.sample(act, Om, Y, Ystride);
+    tm.stop(C.st);
+    to.start(C.st);
+    std::vector<PanelTask> tasks(Ta);
+    for (int a = 0; a < Ta; ++a) {
+      int s = act[a];
+      PanelTask& P = tasks[a];
+      P = PanelTask{};
+      P.Y = Y + s * Ystride;
+      P.Q = Q + s * Qstride;
+      P.R = R + (size_t)s * bs * bs;
+      P.Rp = Rp + (size_t)s * 2 * bs * bs;
+      P.tiny = tiny + (size_t)s * bs;
+      P.deficient = defi + (size_t)s * bs;
+      P.col_norms = cn + (size_t)s * bs;
+      P.new_mass = nm + (size_t)s * bs;
+      P.rng = rng + s;
+      P.rows = S.rows[s];
+      P.width = bs;
+      P.q = q[s];
+    }
+    PanelTask* d_tasks = C.push(tasks);
+    panel_tau(d_tasks, Ta, C.st);
+    ++C.launches;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      // Y <- Y - Q (Q^T Y)  (dense_kernels.cpp:398-401)
+      std::vector<GemmProblem> p1, p2;
+      for (int a = 0; a < Ta; ++a) {
+        int s = act[a];
+        if (q[s] == 0) continue;
+        GemmProblem g{};
+        g.A = Q + s * Qstride; g.lda = S.rows[s]; g.transA = 1;
+        g.B = Y + s * Ystride; g.ldb = S.rows[s];
+        g.C = Cdef + (size_t)s * capmax * bs; g.ldc = q[s];
+        g.M = q[s]; g.N = bs; g.K = S.rows[s]; g.alpha = 1.0;
+        p1.push_back(g);
+        GemmProblem h{};
+        h.A = Q + s * Qstride; h.lda = S.rows[s];
+        h.B = Cdef + (size_t)s * capmax * bs; h.ldb = q[s];
+        h.C = Y + s * Ystride; h.ldc = S.rows[s];
+        h.M = S.rows[s]; h.N = bs; h.K = q[s]; h.alpha = -1.0; h.beta = 1.0;
+        p2.push_back(h);
+      }
+      if (!p1.empty()) {
+        C.gemm(p1);
+        C.gemm(p2);
+      }
+      panel_mgs(d_tasks, Ta, sweep, sweep == 1, bs, maxrows, C.st);
+      ++C.launches;
+    }
+    std::vector<AbsorbTask> ab(Ta);
+    for (int a = 0; a < Ta; ++a) {
+      int s = act[a];
+      AbsorbTask& A = ab[a];
+      A.Y = Y + s * Ystride;
+      A.Q = Q + s * Qstride;
+      A.col_norms = cn + (size_t)s * bs;
+      A.new_mass = nm + (size_t)s * bs;
+      A.recent = recent + (size_t)s * window;
+      A.qcols = qcols + s;
+      A.recent_count = rcount + s;
+      A.recent_pos = rpos + s;
+      A.rounds = rounds + s;
+      A.converged = conv + s;
+      A.done = done + s;
+      A.rows = S.rows[s];
+      A.bs = bs;
+      A.cap = S.cap[s];
+      A.window = window;
+      A.eps = cfg.eps;
+      A.eta = cfg.safety;
+    }
+    ara_absorb(C.push(ab), Ta, C.st);
+    ++C.launches;
+    to.stop(C.st);
+    TLRG_CUDA(cudaMemcpyAsync(h_flags, done, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
+    TLRG_CUDA(cudaMemcpyAsync(h_flags + T, qcols, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
+    C.sync();
+    cst.t_sampling += tm.sec();
+    cst.t_orthog += to.sec();
+    cst.tile_rounds += Ta;
+    for (int a = 0; a < Ta; ++a)
+      if (!S.Sref.empty()) cst.flops_ref += bs * S.Sref[act[a]];
+    std::vector<int> stay;
+    for (int s : act) {
+      q[s] = h_flags[T + s];
+      if (!h_flags[s]) stay.push_back(s);
+    }
+    act.swap(stay);
+  }
+  std::vector<int> h_rounds(T), h_conv(T);
+  TLRG_CUDA(cudaMemcpy(h_rounds.data(), rounds, sizeof(int) * T, cudaMemcpyDeviceToHost));
+  TLRG_CUDA(cudaMemcpy(h_conv.data(), conv, sizeof(int) * T, cudaMemcpyDeviceToHost));
+
+  // ---- exit projection B = E^T Q (ara.cpp:380-387), all tiles at once ------
+  Timer tp, tr;
+  tp.start(C.st);
+  std::vector<long long> boff(T);
+  long long btot = 0;
+  int qmax = 0;
+  for (int s = 0; s < T; ++s) {
+    boff[s] = btot;
+    btot += (long long)cols * q[s];
+    qmax = std::max(qmax, q[s]);
+    if (!S.Sref.empty()) cst.flops_ref += q[s] * S.Sref[s];
+  }
+  double* Bb = C.buf<double>("B", (size_t)std::max(btot, 1LL));
+  op.project(q, Q, Qstride, Bb, boff);
+  tp.stop(C.st);
+
+  // ---- recompression (ara.cpp:201-211) --------------------------------------
+  tr.start(C.st);
+  std::vector<int> fr(T, 0);
+  const double cut = (1.0 - 1.0 / cfg.safety) * cfg.eps;
+  const bool recomp = cfg.recompress && cut > 0.0;
+  std::vector<long long> roff(T);
+  long long rtot = 0;
+  for (int s = 0; s < T; ++s) {
+    roff[s] = rtot;
+    rtot += (long long)q[s] * q[s];
+  }
+  double *Rr = nullptr, *Vs = nullptr;
+  if (recomp && qmax > 0) {
+    Rr = C.buf<double>("Rr", (size_t)rtot + 1);
+    double* Rpr = C.buf<double>("Rpr", (size_t)2 * rtot + 1);
+    Vs = C.buf<double>("Vs", (size_t)rtot + 1);
+    double* work = C.buf<double>("svdwork", (size_t)2 * rtot + 1);
+    double* sig = C.buf<double>("sig", (size_t)T * qmax + 1);
+    double* vec = C.buf<double>("rvec", (size_t)T * qmax * 3 + 1);
+    uint8_t* df = C.buf<uint8_t>("rdef", (size_t)T * qmax + 1);
+    int* rko = C.buf<int>("rank_out", (size_t)T);
+    std::vector<PanelTask> tasks;
+    std::vector<SvdTask> svd;
+    std::vector<int> sl;
+    for (int s = 0; s < T; ++s) {
+      if (q[s] == 0) continue;
+      PanelTask P{};
+      P.Y = Bb + boff[s];
+      P.Q = nullptr;
+      P.R = Rr + roff[s];
+      P.Rp = Rpr + 2 * roff[s];
+      P.tiny = vec + (size_t)s * qmax * 3;
+      P.col_norms = P.tiny + qmax;
+      P.new_mass = P.tiny + 2 * qmax;
+      P.deficient = df + (size_t)s * qmax;
+      P.rng = rng + s;
+      P.rows = cols;
+      P.width = q[s];
+      P.q = 0;
+      tasks.push_back(P);
+      SvdTask V{};
+      V.A = Rr + roff[s];
+      V.V = Vs + roff[s];
+      V.sig = sig + (size_t)s * qmax;
+      V.work = work + 2 * roff[s];
+      V.rank_out = rko + s;
+      V.n = q[s];
+      V.cut = cut;
+      svd.push_back(V);
+      sl.push_back(s);
+    }
+    PanelTask* d_tasks = C.push(tasks);
+    panel_tau(d_tasks, (int)tasks.size(), C.st);
+    panel_mgs(d_tasks, (int)tasks.size(), 0, 0, qmax, cols, C.st);
+    panel_mgs(d_tasks, (int)tasks.size(), 1, 1, qmax, cols, C.st);
+    jacobi_svd(C.push(svd), (int)svd.size(), qmax, C.st);
+    C.launches += 4;
+    std::vector<int> hr(T);
+    TLRG_CUDA(cudaMemcpyAsync(hr.data(), rko, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
+    C.sync();
+    for (int s : sl) fr[s] = hr[s];
+  } else {
+    for (int s = 0; s < T; ++s) fr[s] = q[s];
+  }
+  // ---- final factors into one contiguous panel (in out_order) -------------
+  long long utot = 0, vtot = 0;
+  for (int s : out_order) {
+    utot += (long long)S.rows[s] * fr[s];
+    vtot += (long long)cols * fr[s];
+  }
+  double* Up = utot ? store.alloc((size_t)utot) : nullptr;
+  double* Vp = vtot ? store.alloc((size_t)vtot) : nullptr;
+  std::vector<GemmProblem> pu;
+  std::vector<CopyItem> cpy;
+  long long uo = 0, vo = 0;
+  for (int s : out_order) {
+    out.rank[s] = fr[s];
+    out.rounds[s] = h_rounds[s];
+    out.conv[s] = h_conv[s] != 0;
+    if (fr[s] == 0) continue;
+    out.U[s] = Up + uo;
+    out.V[s] = Vp + vo;
+    uo += (long long)S.rows[s] * fr[s];
+    vo += (long long)cols * fr[s];
+    if (recomp) {
+      // Q <- Q V_s ;  B <- Z (U_s sigma)
+      GemmProblem g{};
+      g.A = Q + s * Qstride; g.lda = S.rows[s];
+      g.B = Vs + roff[s]; g.ldb = q[s];
+      g.C = out.U[s]; g.ldc = S.rows[s];
+      g.M = S.rows[s]; g.N = fr[s]; g.K = q[s]; g.alpha = 1.0;
+      pu.push_back(g);
+      GemmProblem h{};
+      h.A = Bb + boff[s]; h.lda = cols;
+      h.B = Rr + roff[s]; h.ldb = q[s];
+      h.C = out.V[s]; h.ldc = cols;
+      h.M = cols; h.N = fr[s]; h.K = q[s]; h.alpha = 1.0;
+      pu.push_back(h);
+    } else {
+      cpy.push_back({Q + s * Qstride, out.U[s], S.rows[s], S.rows[s], S.rows[s], fr[s]});
+      cpy.push_back({Bb + boff[s], out.V[s], cols, cols, cols, fr[s]});
+    }
+  }
+  if (!pu.empty()) C.gemm(pu);
+  if (!cpy.empty()) {
+    batched_copy(C.push(cpy), (int)cpy.size(), C.st);
+    ++C.launches;
+  }
+  tr.stop(C.st);
+  C.sync();
+  cst.t_projection += tp.sec();
+  cst.t_recompress += tr.sec();
+}
+
+}  // namespace tlrg

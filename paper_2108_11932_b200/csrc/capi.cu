@@ -841,10 +841,15 @@ int tlrg_gemm(tlrg_ctx ctx, int32_t M, int32_t N, int32_t K, int32_t ta, int32_t
   });
 }
 
-int tlrg_build(tlrg_ctx, int32_t, int64_t, const double*, int32_t, double, double, int32_t, double,
-               int32_t, const tlrg_ara_config*, tlrg_matrix*, tlrg_status* st) {
-  set_status(st, 2, "tlrg_build: construction on device not implemented yet");
-  return 2;
+int tlrg_build(tlrg_ctx ctx, int32_t dim, int64_t n, const double* coords, int32_t kernel_kind,
+               double ell, double nugget, int32_t b, double eps, int32_t compressor,
+               const tlrg_ara_config* cfg, tlrg_matrix* out, tlrg_status* st) {
+  return guarded(st, [&] {
+    auto* h = new tlrg_matrix_s;
+    h->m = build_tlr_device(ctx->c, dim, n, coords, kernel_kind, ell, nugget, b, eps, compressor,
+                            to_cfg(cfg));
+    *out = h;
+  });
 }
 
 }  // extern "C"

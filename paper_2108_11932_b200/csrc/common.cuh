@@ -64,4 +64,18 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Opt a kernel into the largest dynamic shared memory the device allows
+// (opt-in limit minus the kernel's static shared memory).  Returns the limit.
+template <class K>
+inline size_t enable_max_dyn_smem(K kernel) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, kernel);
+  size_t lim = (size_t)optin - fa.sharedSizeBytes;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+  return lim;
+}
+
 }  // namespace tlrg

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -164,6 +165,28 @@ void column_setup(Ctx& C, const Matrix& M, int k, const DBlocks& D, ColumnSetup&
 void column_H(Ctx& C, const Matrix& M, const ColumnSetup& cs, const std::vector<int>& targets,
               double* H, long long stride);
 
+// Generic batched ARA (ara.cu).  Slot s is one tile: rows(s) x cols operator.
+struct AraSlots {
+  std::vector<int> rows, cap;
+  std::vector<uint64_t> seeds;
+  std::vector<double> Sref;  // reference flops per sampled vector (optional)
+  int cols = 0;
+};
+struct AraOperator {
+  // enqueue Y_s = E_s Omega_a for the active slots (Omega_a at Om + a*cols*bs)
+  std::function<void(const std::vector<int>& act, const double* Om, double* Y,
+                     long long Ystride)> sample;
+  // enqueue B_s = E_s^T Q_s (cols x q_s, ld cols) at Bb + boff[s] for q_s > 0
+  std::function<void(const std::vector<int>& q, const double* Q, long long Qstride, double* Bb,
+                     const std::vector<long long>& boff)> project;
+};
+struct AraOut {
+  std::vector<int> rank, rounds, conv;
+  std::vector<double*> U, V;
+};
+void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,
+               const std::vector<int>& out_order, ColumnStats& cst, AraOut& out);
+
 // Dynamic-batched ARA over column k (chol_ara_update, ara.cpp:302-419): all
 // non-trivial tiles resident, converged tiles leave, exit projection and SVD
 // recompression batched at the end.  Results (ascending i) land in a panel
@@ -198,6 +221,11 @@ struct Factor {
 
 std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, const AraCfg& cfg,
                                   int parallel_buffers, const FactorOpts& opts);
+
+// build_tlr (tlr_matrix.cpp:98-152) on the device; coords in matrix order.
+std::unique_ptr<Matrix> build_tlr_device(Ctx& C, int dim, int64_t n, const double* coords_host,
+                                         int kind, double ell, double nugget, int b, double eps,
+                                         int compressor, const AraCfg& cfg);
 
 // dense building blocks on device memory
 bool potrf_device(Ctx& C, double* A, int n);  // returns success

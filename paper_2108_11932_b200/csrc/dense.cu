@@ -416,12 +416,8 @@ void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* pe
                 cudaStream_t st) {
   if (nrhs <= 0 || n <= 0) return;
   size_t bytes = (size_t)n * TR_C * 8;
-  static bool configured = false;
-  if (bytes > 48 * 1024 && !configured) {
-    TLRG_CUDA(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-    configured = true;
-  }
+  static size_t lim = enable_max_dyn_smem(trsm_panel_kernel);
+  if (bytes > lim) throw CudaError("trsm_panel: tile too large for shared memory");
   unsigned blocks = (unsigned)((nrhs + TR_C - 1) / TR_C);
   trsm_panel_kernel<<<blocks, 256, bytes, st>>>(L, n, B, nrhs, perm, d, e, s2, info);
   TLRG_CUDA(cudaGetLastError());

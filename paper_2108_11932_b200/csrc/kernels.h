@@ -83,10 +83,11 @@ struct SvdTask {
   double* sig; // n (sorted descending on exit)
   double* work; // 2 n^2 scratch, used when the problem does not fit in smem
   int* rank_out;
-  int n;
+  int n;        // columns (V is n x n)
   double cut;
+  int m;        // rows of A (0 = n)
 };
-void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st);
+void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m = 0);
 
 // Block-diagonal product H[:, seg_j] = U_ij * G_ij for a set of (tile, j) items.
 struct BlockItem {

@@ -231,14 +231,9 @@ void panel_mgs(PanelTask* d_tasks, int ntask, int sweep, int finalize, int max_w
   int cbuf_len = max_width > max_rows ? max_width : max_rows;
   size_t base = (size_t)(cbuf_len + 32 + MT_N) * 8;
   size_t ys = (size_t)max_rows * max_width * 8;
-  int in_smem = base + ys <= 200 * 1024;
+  static size_t lim = enable_max_dyn_smem(panel_mgs_kernel);
+  int in_smem = base + ys <= lim;
   size_t bytes = base + (in_smem ? ys : 0);
-  static size_t configured = 0;
-  if (bytes > 48 * 1024 && bytes > configured) {
-    TLRG_CUDA(cudaFuncSetAttribute(panel_mgs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-    configured = 227 * 1024;
-  }
   panel_mgs_kernel<<<ntask, PT, bytes, st>>>(d_tasks, sweep, finalize, in_smem, cbuf_len);
   TLRG_CUDA(cudaGetLastError());
 }
@@ -296,17 +291,16 @@ constexpr int JT = 256;
 __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int staged) {
   extern __shared__ double jsm[];
   SvdTask& T = tasks[blockIdx.x];
-  const int n = T.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = JT / 32;
+  const int n = T.n, m = T.m > 0 ? T.m : T.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = JT / 32;
   if (n == 0) {
     if (tid == 0) *T.rank_out = 0;
     return;
   }
-  double* A = staged ? jsm : T.work;
-  double* V = A + (long long)n * n;
-  for (long long e = tid; e < (long long)n * n; e += JT) {
-    A[e] = T.A[e];
-    V[e] = (e % n == e / n) ? 1.0 : 0.0;
-  }
+  double* A = staged ? jsm : T.work;       // m x n
+  double* V = A + (long long)m * n;        // n x n
+  for (long long e = tid; e < (long long)m * n; e += JT) A[e] = T.A[e];
+  for (long long e = tid; e < (long long)n * n; e += JT) V[e] = (e % n == e / n) ? 1.0 : 0.0;
   __shared__ int rotated;
   __syncthreads();
   const int nn = n + (n & 1);
@@ -318,10 +312,10 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
         int p = (step + pi) % (nn - 1);
         int q = pi == 0 ? nn - 1 : (step - pi + nn - 1) % (nn - 1);
         if (p >= n || q >= n) continue;
-        double* ap = A + (long long)p * n;
-        double* aq = A + (long long)q * n;
+        double* ap = A + (long long)p * m;
+        double* aq = A + (long long)q * m;
         double al = 0, be = 0, ga = 0;
-        for (int r = lane; r < n; r += 32) {
+        for (int r = lane; r < m; r += 32) {
           al += ap[r] * ap[r];
           be += aq[r] * aq[r];
           ga += ap[r] * aq[r];
@@ -333,7 +327,7 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
           double zeta = (be - al) / (2.0 * ga);
           double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int r = lane; r < n; r += 32) {
+          for (int r = lane; r < m; r += 32) {
             double x = ap[r], y = aq[r];
             ap[r] = c * x - s * y;
             aq[r] = s * x + c * y;
@@ -356,7 +350,7 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   // singular values = column norms of A
   for (int p = warp; p < n; p += nw) {
     double s = 0.0;
-    for (int r = lane; r < n; r += 32) s += A[(long long)p * n + r] * A[(long long)p * n + r];
+    for (int r = lane; r < m; r += 32) s += A[(long long)p * m + r] * A[(long long)p * m + r];
     s = warp_sum(s);
     if (lane == 0) T.sig[p] = sqrt(s);
   }
@@ -373,25 +367,26 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
     }
     rk = warp_sum_int(rk);
     if (lane == 0 && sp > T.cut) atomicAdd(&cnt, 1);
-    for (int r = lane; r < n; r += 32) {
-      T.A[(long long)rk * n + r] = A[(long long)p * n + r];
-      T.V[(long long)rk * n + r] = V[(long long)p * n + r];
-    }
+    for (int r = lane; r < m; r += 32) T.A[(long long)rk * m + r] = A[(long long)p * m + r];
+    for (int r = lane; r < n; r += 32) T.V[(long long)rk * n + r] = V[(long long)p * n + r];
   }
   __syncthreads();
+  // sigma in descending order
+  for (int p = warp; p < n; p += nw) {
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s += T.A[(long long)p * m + r] * T.A[(long long)p * m + r];
+    s = warp_sum(s);
+    if (lane == 0) T.sig[p] = sqrt(s);
+  }
   if (tid == 0) *T.rank_out = cnt;
 }
 
-void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st) {
+void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m) {
   if (ntask <= 0) return;
-  size_t bytes = (size_t)2 * max_n * max_n * 8;
-  int staged = bytes <= 200 * 1024;
-  static bool configured = false;
-  if (staged && bytes > 48 * 1024 && !configured) {
-    TLRG_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-    configured = true;
-  }
+  if (max_m <= 0) max_m = max_n;
+  size_t bytes = ((size_t)max_m * max_n + (size_t)max_n * max_n) * 8;
+  static size_t lim = enable_max_dyn_smem(jacobi_svd_kernel);
+  int staged = bytes <= lim;
   jacobi_svd_kernel<<<ntask, JT, staged ? bytes : 16, st>>>(d_tasks, staged);
   TLRG_CUDA(cudaGetLastError());
 }

@@ -583,3 +583,18 @@ def gemm(alpha, A, ta, B, tb, beta=0.0, Cm=None, ctx=None):
     _call(ctx.lib.tlrg_gemm, ctx.h, M, N, K, int(ta), int(tb), alpha, A.ctypes.data_as(L.dp),
           B.ctypes.data_as(L.dp), beta, Cm.ctypes.data_as(L.dp))
     return np.array(Cm)
+
+
+def build_tlr(coords, kernel_kind, ell, nugget, b, eps, compressor=0, cfg: AraConfig = None,
+              ctx=None) -> TlrMatrix:
+    """build_tlr (tlr_matrix.cpp:98-152) on the device.  ``coords`` are the points
+    in matrix order, shape (N, dim) (see geometry.kd_order(...).matrix_order()).
+    kernel_kind 0 = exp(-r/ell), 1 = exp(-r^2/(2 ell^2)); compressor 0 ARA, 1 SVD."""
+    ctx = _ctx(ctx)
+    X = _f64(coords)
+    cfg = cfg or AraConfig()
+    c = cfg.c()
+    h = C.c_void_p()
+    _call(ctx.lib.tlrg_build, ctx.h, X.shape[1], X.shape[0], _d(X), kernel_kind, ell, nugget, b,
+          eps, compressor, C.byref(c), C.byref(h))
+    return TlrMatrix(h, ctx)

@@ -102,3 +102,24 @@ def test_solve_apply_matvec_match_reference(tg, ref):
     b = A_ref.matvec(x)
     xs = tg.factor_solve(F, b)
     assert np.linalg.norm(A_ref.matvec(xs) - b) / np.linalg.norm(b) <= 100 * F.L.nb * eps
+
+
+@pytest.mark.parametrize("kind,n,b,eps,kernel,nugget,comp", [
+    (G.GRID2D, 1024, 128, 1e-6, 0, 0.0, 0), (G.BALL3D, 768, 128, 1e-4, 1, 1e-4, 0),
+    (G.GRID2D, 500, 128, 1e-5, 0, 0.0, 0), (G.BALL3D, 384, 96, 1e-5, 0, 0.0, 1)])
+def test_device_build_matches_reference_build(tg, ref, kind, n, b, eps, kernel, nugget, comp):
+    """build_tlr on the device with the reference's per-tile seeds (0xb11d)."""
+    from paper_2108_11932_b200.tlr import build_tlr
+    pts = points(kind, n, b, 42 if kind == G.BALL3D else 0)
+    ell = 0.1 if kind == G.GRID2D else 0.2
+    A = build_tlr(pts, kernel, ell, nugget, b, eps, compressor=comp,
+                  cfg=tg.AraConfig(block_samples=16, seed=9))
+    A_ref = ref.build(pts, kernel, ell, nugget, b, eps, comp, 16, 9)
+    rk, rkr = A.ranks(), A_ref.ranks()
+    assert (rk == rkr).mean() >= 0.97
+    d1, _, U1, V1 = A.to_parts()
+    d2, _, U2, V2 = A_ref.to_parts()
+    for x, y in zip(d1, d2):
+        assert np.abs(x - y).max() <= 1e-15
+    for u1, v1, u2, v2 in zip(U1, V1, U2, V2):
+        assert np.abs(u1 @ v1.T - u2 @ v2.T).max() <= 2 * eps
