@@ -88,6 +88,14 @@ __global__ void __launch_bounds__(128) potrf_panel_kernel(double* A, int n, int 
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
 
+// dense_kernels.cpp:79-80: the returned factor has an exactly zero upper part
+__global__ void zero_upper_kernel(double* A, int n) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)n * n) return;
+  int i = (int)(t % n), j = (int)(t / n);
+  if (i < j) A[t] = 0.0;
+}
+
 void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st) {
   set_int_kernel<<<1, 1, 0, st>>>(info, -1);
   for (int p0 = 0; p0 < n; p0 += PB) {
@@ -116,6 +124,9 @@ void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st) {
     potrf_panel_kernel<<<blocks, 128, 0, st>>>(A, n, p0, pw, info);
     TLRG_CUDA(cudaGetLastError());
   }
+  long long nn = (long long)n * n;
+  zero_upper_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(A, n);
+  TLRG_CUDA(cudaGetLastError());
 }
 
 // ------------------------------------------------------ BUNCH-KAUFMAN -----
