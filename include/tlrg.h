@@ -63,6 +63,10 @@ typedef struct {
   double flops_exec;         /* FP64 flops executed by the GEMM phases */
   double flops_gemm_ref;     /* reference-formulation F_gemm */
   int64_t kernel_launches;   /* device kernels launched by the factorization */
+  double t_device;           /* CUDA-event time of the whole factorization (s) */
+  double kt_gemm_seconds;    /* summed grouped-GEMM launch time (TLRG_KTIMING=1) */
+  double kt_gemm_flops;      /* flops of those launches */
+  int64_t kt_gemm_launches;
 } tlrg_stats;
 
 typedef struct {

@@ -40,7 +40,9 @@ class StatsC(C.Structure):
                 ("compensation_frob", C.c_double), ("modified_diagonals", C.c_int32),
                 ("tile_rounds_resident", C.c_uint64), ("t_recompress", C.c_double),
                 ("t_compensation", C.c_double), ("flops_exec", C.c_double),
-                ("flops_gemm_ref", C.c_double), ("kernel_launches", C.c_int64)]
+                ("flops_gemm_ref", C.c_double), ("kernel_launches", C.c_int64),
+                ("t_device", C.c_double), ("kt_gemm_seconds", C.c_double),
+                ("kt_gemm_flops", C.c_double), ("kt_gemm_launches", C.c_int64)]
 
 
 class StatusC(C.Structure):

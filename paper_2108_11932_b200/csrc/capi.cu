@@ -159,7 +159,7 @@ std::unique_ptr<Matrix> clone(Ctx& C, const Matrix& M) {
   R->V.assign(M.V.size(), nullptr);
   size_t dbytes = sizeof(double) * (size_t)M.nb * M.b * M.b;
   TLRG_CUDA(cudaMalloc(&R->diag, dbytes));
-  TLRG_CUDA(cudaMemcpy(R->diag, M.diag, dbytes, cudaMemcpyDeviceToDevice));
+  TLRG_CUDA(cudaMemcpyAsync(R->diag, M.diag, dbytes, cudaMemcpyDeviceToDevice, C.st));
   size_t tot = 0;
   for (int i = 1; i < M.nb; ++i)
     for (int j = 0; j < i; ++j) {
@@ -442,6 +442,10 @@ int tlrg_factor_stats(tlrg_factor f, tlrg_stats* o, int32_t* ara_rounds, double*
     o->flops_exec = S.flops_exec;
     o->flops_gemm_ref = S.flops_ref;
     o->kernel_launches = S.launches;
+    o->t_device = S.t_device;
+    o->kt_gemm_seconds = S.kt_gemm_seconds;
+    o->kt_gemm_flops = S.kt_gemm_flops;
+    o->kt_gemm_launches = S.kt_gemm_launches;
   }
   int nb = f->f->L->nb;
   if (ara_rounds)
@@ -535,12 +539,7 @@ static double power_iter(Ctx& C, int64_t n, uint64_t seed0, int iters,
   rng_seed(rs, C.push(s1), 1, C.st);
   rng_draw(rs, nullptr, 1, v, n, n, C.st);
   double nv = std::sqrt(dot_device(C, v, v, n));
-  std::vector<double> hv(n);
-  auto scale = [&](double* p, double s) {
-    TLRG_CUDA(cudaMemcpy(hv.data(), p, 8 * n, cudaMemcpyDeviceToHost));
-    for (auto& t : hv) t *= s;
-    TLRG_CUDA(cudaMemcpy(p, hv.data(), 8 * n, cudaMemcpyHostToDevice));
-  };
+  auto scale = [&](double* p, double s) { axpby_device(C, 0.0, p, s, p, n); };
   scale(v, 1.0 / nv);
   double lambda = 0.0;
   for (int t = 0; t < iters; ++t) {
@@ -564,14 +563,7 @@ int tlrg_estimate_2norm_diff(tlrg_matrix A, tlrg_factor f, int32_t iters, uint64
     *out = power_iter(C, n, mix64(seed ^ 0x2fULL), iters, [&](const double* v, double* w) {
       matvec_device(C, *A->m, v, w);
       factor_apply_device(C, *f->f, v, t);
-      std::vector<GemmProblem> none;
-      // w -= t  (use a 1-column GEMM-free axpy via dot helpers: do it on host side)
-      std::vector<double> hw(n), ht(n);
-      TLRG_CUDA(cudaMemcpyAsync(hw.data(), w, 8 * n, cudaMemcpyDeviceToHost, C.st));
-      TLRG_CUDA(cudaMemcpyAsync(ht.data(), t, 8 * n, cudaMemcpyDeviceToHost, C.st));
-      C.sync();
-      for (int64_t i = 0; i < n; ++i) hw[i] -= ht[i];
-      TLRG_CUDA(cudaMemcpy(w, hw.data(), 8 * n, cudaMemcpyHostToDevice));
+      axpby_device(C, -1.0, t, 1.0, w, n);  // w = A v - L L^T v  (difference_apply)
     });
   });
 }

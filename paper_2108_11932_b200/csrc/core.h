@@ -67,6 +67,12 @@ struct Ctx {
   size_t h_dbl_cap = 0;
   double flops = 0.0;
   long long launches = 0;
+  // optional per-launch CUDA-event timing of the grouped GEMM (TLRG_KTIMING=1)
+  bool ktiming = false;
+  double kt_seconds = 0.0, kt_flops = 0.0;
+  long long kt_launches = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<std::pair<cudaEvent_t, cudaEvent_t>, double>> ev_pending;
 
   template <class T>
   T* buf(const std::string& name, size_t count) {
@@ -74,10 +80,33 @@ struct Ctx {
   }
   int* pinned_ints(size_t n);
   double* pinned_dbl(size_t n);
+  cudaEvent_t take_event() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      TLRG_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  void drain_events() {
+    for (auto& p : ev_pending) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, p.first.first, p.first.second);
+      kt_seconds += ms * 1e-3;
+      kt_flops += p.second;
+      ++kt_launches;
+      ev_pool.push_back(p.first.first);
+      ev_pool.push_back(p.first.second);
+    }
+    ev_pending.clear();
+  }
   void sync() {
     TLRG_CUDA(cudaStreamSynchronize(st));
     desc.reset();
     release_retired_arenas();
+    if (!ev_pending.empty()) drain_events();
   }
   template <class T>
   T* push(const std::vector<T>& v) {
@@ -85,9 +114,19 @@ struct Ctx {
     return static_cast<T*>(desc.push(v.data(), v.size() * sizeof(T), st));
   }
   void gemm(std::vector<GemmProblem>& probs) {
+    double f = 0.0;
     for (auto& p : probs)
-      if (p.M > 0 && p.N > 0) flops += 2.0 * p.M * p.N * p.K;
-    grouped_gemm(probs, desc, st);
+      if (p.M > 0 && p.N > 0) f += 2.0 * p.M * p.N * p.K;
+    flops += f;
+    if (ktiming && f > 0) {
+      cudaEvent_t a = take_event(), b = take_event();
+      TLRG_CUDA(cudaEventRecord(a, st));
+      grouped_gemm(probs, desc, st);
+      TLRG_CUDA(cudaEventRecord(b, st));
+      ev_pending.push_back({{a, b}, f});
+    } else {
+      grouped_gemm(probs, desc, st);
+    }
     ++launches;
   }
   ~Ctx();
@@ -205,6 +244,9 @@ struct Stats {
   int modified_diagonals = 0;
   uint64_t tile_rounds_resident = 0;
   double t_recompress = 0, t_compensation = 0, flops_exec = 0, flops_ref = 0;
+  double t_device = 0;        // CUDA-event time of the whole factorization
+  double kt_gemm_seconds = 0, kt_gemm_flops = 0;  // per-launch GEMM timing (KTIMING)
+  long long kt_gemm_launches = 0;
   long long launches = 0;
   std::vector<int> ara_rounds;
   std::vector<double> pivot_trace;
@@ -239,5 +281,7 @@ void matvec_device(Ctx& C, const Matrix& A, const double* x, double* y);
 void factor_apply_device(Ctx& C, const Factor& F, const double* x, double* y);
 void factor_solve_device(Ctx& C, const Factor& F, double* x);  // in place
 double dot_device(Ctx& C, const double* a, const double* b, long long n);
+// y <- a*x + b*y on C.st
+void axpby_device(Ctx& C, double a, const double* x, double b, double* y, long long n);
 
 }  // namespace tlrg

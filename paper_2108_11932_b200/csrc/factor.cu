@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "core.h"
@@ -279,6 +280,12 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   auto t_wall0 = std::chrono::steady_clock::now();
   double flops0 = C.flops;
   long long launches0 = C.launches;
+  const char* kt = std::getenv("TLRG_KTIMING");
+  C.ktiming = kt && kt[0] == '1';
+  C.kt_seconds = C.kt_flops = 0.0;
+  C.kt_launches = 0;
+  Ev d0, d1;
+  cudaEventRecord(d0.e, C.st);
 
   auto F = std::make_unique<Factor>();
   F->mode = mode;
@@ -417,6 +424,13 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     C.sync();
     S.t_misc += elapsed(e4, e5);
   }
+  cudaEventRecord(d1.e, C.st);
+  C.sync();
+  S.t_device = elapsed(d0, d1);
+  S.kt_gemm_seconds = C.kt_seconds;
+  S.kt_gemm_flops = C.kt_flops;
+  S.kt_gemm_launches = C.kt_launches;
+  C.ktiming = false;
   TLRG_CUDA(cudaMemcpy(S.pivot_trace.data(), piv, sizeof(double) * nb, cudaMemcpyDeviceToHost));
   S.wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_wall0).count();
   S.flops_exec = C.flops - flops0;

@@ -260,6 +260,20 @@ void launch_dots(Ctx& C, const std::vector<DotItem>& it, const double* x, double
 
 }  // namespace
 
+namespace {
+__global__ void axpby_kernel(double a, const double* x, double b, double* y, long long n) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x)
+    y[t] = (a != 0.0 ? a * x[t] : 0.0) + b * y[t];
+}
+}  // namespace
+
+void axpby_device(Ctx& C, double a, const double* x, double b, double* y, long long n) {
+  int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  axpby_kernel<<<blocks, 256, 0, C.st>>>(a, x, b, y, n);
+  TLRG_CUDA(cudaGetLastError());
+}
+
 double dot_device(Ctx& C, const double* a, const double* b, long long n) {
   int blocks = (int)std::min<long long>((n + 255) / 256, 296);
   double* part = C.buf<double>("dot_part", 300);

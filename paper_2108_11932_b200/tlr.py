@@ -297,6 +297,10 @@ class FactorStats:
     flops_exec: float = 0
     flops_gemm_ref: float = 0
     kernel_launches: int = 0
+    t_device: float = 0
+    kt_gemm_seconds: float = 0
+    kt_gemm_flops: float = 0
+    kt_gemm_launches: int = 0
     ara_rounds: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
     pivot_trace: np.ndarray = field(default_factory=lambda: np.zeros(0))
 
