@@ -8,125 +8,140 @@
 //   * small helpers: symmetrize, diagonal combine, pivot traces, D apply.
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace tlrg {
 
 // ---------------------------------------------------------------- POTRF ---
-constexpr int PB = 32;  // panel width
+// Left-looking blocked Cholesky in ONE cooperative kernel: CTA r owns the
+// 32-row block r.  Per 32-column panel p:
+//   update : A[r, p] -= L[r, 0:p] L[p, 0:p]^T      (CTAs r >= p, in parallel)
+//   grid.sync
+//   factor : every CTA factors A_pp redundantly in shared memory (one warp),
+//            CTA p stores L_pp, CTAs r > p solve X L_pp^T = A[r, p]
+//   grid.sync
+constexpr int PB = 32;
+constexpr int PO_T = 128;
 
-// CTA per 32-row block r >= p: factor the (already updated) diagonal block
-// A_pp in shared memory, then either store L_pp or solve X L_pp^T = A_rp.
-__global__ void __launch_bounds__(128) potrf_panel_kernel(double* A, int n, int p0, int pw,
-                                                          int* info) {
+__global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int* info) {
+  cg::grid_group grid = cg::this_grid();
   __shared__ double Lp[PB][PB + 1];
-  __shared__ double Ar[128][PB + 1];
+  __shared__ double Ar[PB][PB + 1];
+  __shared__ double La[PB][PB + 1];
+  __shared__ double Lb[PB][PB + 1];
   __shared__ int fail;
   const int tid = threadIdx.x, lane = tid & 31;
+  const int r = blockIdx.x;            // row block
+  const int r0 = r * PB;
+  const int rw = min(PB, n - r0);
+  const int np = (n + PB - 1) / PB;
   if (tid == 0) fail = -1;
-  for (int e = tid; e < PB * PB; e += 128) {
-    int i = e % PB, j = e / PB;
-    Lp[i][j] = (i < pw && j < pw) ? A[(p0 + i) + (long long)(p0 + j) * n] : 0.0;
-  }
-  __syncthreads();
-  if (tid < 32) {
-    // unblocked right-looking Cholesky of the pw x pw block (one warp)
-    for (int j = 0; j < pw; ++j) {
-      double d = Lp[j][j];
-      bool bad = !(d > 0.0);
-      if (bad) {
-        if (lane == 0) fail = j;
-        break;
+  for (int p = 0; p < np; ++p) {
+    const int p0 = p * PB, pw = min(PB, n - p0);
+    if (r >= p) {
+      // ---- update A[r, p] -= L[r, 0:p0] L[p, 0:p0]^T (thread: 8 outputs) ----
+      double acc[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] = 0.0;
+      const int ci = tid & 31, rj = tid >> 5;  // column ci of the block, rows rj + 4t
+      for (int k0 = 0; k0 < p0; k0 += PB) {
+        for (int e = tid; e < PB * PB; e += PO_T) {
+          int i = e % PB, k = e / PB;
+          La[i][k] = i < rw ? A[(r0 + i) + (long long)(k0 + k) * n] : 0.0;
+          Lb[i][k] = i < pw ? A[(p0 + i) + (long long)(k0 + k) * n] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < PB; ++k) {
+          double bv = Lb[ci][k];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) acc[t] += La[rj + 4 * t][k] * bv;
+        }
+        __syncthreads();
       }
-      double s = sqrt(d);
-      __syncwarp();
-      if (lane == 0) Lp[j][j] = s;
-      __syncwarp();
-      if (lane > j && lane < pw) Lp[lane][j] /= s;
-      __syncwarp();
-      if (lane > j && lane < pw)
-        for (int c = j + 1; c <= lane; ++c) Lp[lane][c] -= Lp[lane][j] * Lp[c][j];
-      __syncwarp();
+      if (p0 > 0)
+        for (int t = 0; t < 8; ++t) {
+          int i = rj + 4 * t;
+          if (i < rw && ci < pw) A[(r0 + i) + (long long)(p0 + ci) * n] -= acc[t];
+        }
     }
-  }
-  __syncthreads();
-  if (fail >= 0) {
-    if (tid == 0 && blockIdx.x == 0) atomicCAS(info, -1, p0 + fail);
-    return;
-  }
-  const int rb0 = p0 + blockIdx.x * 128;  // first row handled by this CTA
-  if (blockIdx.x == 0) {
-    // diagonal block rows [p0, p0+pw): store L_pp (zero the strict upper part)
-    for (int e = tid; e < pw * pw; e += 128) {
-      int i = e % pw, j = e / pw;
-      A[(p0 + i) + (long long)(p0 + j) * n] = i >= j ? Lp[i][j] : 0.0;
+    grid.sync();
+    if (r >= p) {
+      for (int e = tid; e < PB * PB; e += PO_T) {
+        int i = e % PB, j = e / PB;
+        Lp[i][j] = (i < pw && j < pw) ? A[(p0 + i) + (long long)(p0 + j) * n] : 0.0;
+      }
+      __syncthreads();
+      if (tid < 32) {
+        for (int j = 0; j < pw; ++j) {
+          double d = Lp[j][j];
+          if (!(d > 0.0)) {
+            if (lane == 0) fail = p0 + j;
+            break;
+          }
+          double s = sqrt(d);
+          __syncwarp();
+          if (lane == 0) Lp[j][j] = s;
+          __syncwarp();
+          if (lane > j && lane < pw) Lp[lane][j] /= s;
+          __syncwarp();
+          if (lane > j && lane < pw)
+            for (int c = j + 1; c <= lane; ++c) Lp[lane][c] -= Lp[lane][j] * Lp[c][j];
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (fail < 0) {
+        if (r == p) {
+          for (int e = tid; e < pw * pw; e += PO_T) {
+            int i = e % pw, j = e / pw;
+            A[(p0 + i) + (long long)(p0 + j) * n] = i >= j ? Lp[i][j] : 0.0;
+          }
+        } else {
+          for (int e = tid; e < rw * pw; e += PO_T) {
+            int i = e % rw, j = e / rw;
+            Ar[i][j] = A[(r0 + i) + (long long)(p0 + j) * n];
+          }
+          __syncthreads();
+          if (tid < rw)
+            for (int j = 0; j < pw; ++j) {
+              double s = Ar[tid][j];
+              for (int t = 0; t < j; ++t) s -= Ar[tid][t] * Lp[j][t];
+              Ar[tid][j] = s / Lp[j][j];
+            }
+          __syncthreads();
+          for (int e = tid; e < rw * pw; e += PO_T) {
+            int i = e % rw, j = e / rw;
+            A[(r0 + i) + (long long)(p0 + j) * n] = Ar[i][j];
+          }
+        }
+      }
     }
+    // every CTA that factored A_pp agrees on failure; CTA p reports it
+    if (r == p && tid == 0 && fail >= 0) atomicCAS(info, -1, fail);
+    grid.sync();
+    if (*(volatile int*)info >= 0) break;
   }
-  // rows below the diagonal block that this CTA owns: [max(rb0, p0+pw), rb0+128)
-  int r_lo = rb0 < p0 + pw ? p0 + pw : rb0;
-  int r_hi = rb0 + 128 < n ? rb0 + 128 : n;
-  int nr = r_hi - r_lo;
-  if (nr <= 0) return;
-  for (int e = tid; e < nr * pw; e += 128) {
-    int i = e % nr, j = e / nr;
-    Ar[i][j] = A[(r_lo + i) + (long long)(p0 + j) * n];
-  }
-  __syncthreads();
-  if (tid < nr) {
-    for (int j = 0; j < pw; ++j) {
-      double s = Ar[tid][j];
-      for (int t = 0; t < j; ++t) s -= Ar[tid][t] * Lp[j][t];
-      Ar[tid][j] = s / Lp[j][j];
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < nr * pw; e += 128) {
-    int i = e % nr, j = e / nr;
-    A[(r_lo + i) + (long long)(p0 + j) * n] = Ar[i][j];
+  // zero the strict upper triangle of this row block (dense_kernels.cpp:79-80)
+  for (long long e = tid; e < (long long)rw * n; e += PO_T) {
+    int i = (int)(e % rw), j = (int)(e / rw);
+    if (r0 + i < j) A[(r0 + i) + (long long)j * n] = 0.0;
   }
 }
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
 
-// dense_kernels.cpp:79-80: the returned factor has an exactly zero upper part
-__global__ void zero_upper_kernel(double* A, int n) {
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= (long long)n * n) return;
-  int i = (int)(t % n), j = (int)(t / n);
-  if (i < j) A[t] = 0.0;
-}
-
 void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st) {
+  (void)desc;
   set_int_kernel<<<1, 1, 0, st>>>(info, -1);
-  for (int p0 = 0; p0 < n; p0 += PB) {
-    int pw = n - p0 < PB ? n - p0 : PB;
-    if (p0 > 0) {
-      // A[p0:, p0:p0+pw] -= L[p0:, 0:p0] * L[p0:p0+pw, 0:p0]^T
-      std::vector<GemmProblem> pr(1);
-      GemmProblem& g = pr[0];
-      g.A = A + p0;
-      g.lda = n;
-      g.transA = 0;
-      g.B = A + p0;
-      g.ldb = n;
-      g.transB = 1;
-      g.C = A + p0 + (long long)p0 * n;
-      g.ldc = n;
-      g.M = n - p0;
-      g.N = pw;
-      g.K = p0;
-      g.alpha = -1.0;
-      g.beta = 1.0;
-      grouped_gemm(pr, desc, st);
-    }
-    int rows = n - p0;
-    int blocks = (rows + 127) / 128;
-    potrf_panel_kernel<<<blocks, 128, 0, st>>>(A, n, p0, pw, info);
-    TLRG_CUDA(cudaGetLastError());
-  }
-  long long nn = (long long)n * n;
-  zero_upper_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(A, n);
-  TLRG_CUDA(cudaGetLastError());
+  int nblk = (n + PB - 1) / PB;
+  void* args[] = {&A, &n, &info};
+  TLRG_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel, dim3(nblk), dim3(PO_T), args, 0,
+                                        st));
 }
 
 // ------------------------------------------------------ BUNCH-KAUFMAN -----
@@ -345,48 +360,60 @@ void sytrf_bk(double* A, int n, double* d, double* e, uint8_t* s2, int* perm, in
 }
 
 // ----------------------------------------------------------------- TRSM ---
-// X = L^{-1} B for a panel of right-hand sides; one CTA per 16 columns.
+// X = L^{-1} B for a panel of right-hand sides; one CTA per TR_C columns, X in
+// shared memory, L streamed through shared memory in 32 x 32 blocks.
 // LDL mode (perm != null): rows are gathered through perm, L is unit lower and
 // the block diagonal D^{-1} is applied last (factor.cpp:257-262).
-constexpr int TR_C = 16;
+constexpr int TR_C = 8;
+constexpr int TR_T = 256;
 
-__global__ void __launch_bounds__(256) trsm_panel_kernel(const double* L, int n, double* B,
-                                                         long long nrhs, const int* perm,
-                                                         const double* d, const double* e,
-                                                         const uint8_t* s2, int* info) {
+__global__ void __launch_bounds__(TR_T) trsm_panel_kernel(const double* L, int n, double* B,
+                                                          long long nrhs, const int* perm,
+                                                          const double* d, const double* e,
+                                                          const uint8_t* s2, int* info) {
   extern __shared__ double X[];  // n x TR_C, ld n
+  __shared__ double Ls[32][33];
   const long long c0 = (long long)blockIdx.x * TR_C;
   const int nc = (int)(nrhs - c0 < TR_C ? nrhs - c0 : TR_C);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool unit = perm != nullptr;
-  for (int t = tid; t < n * nc; t += 256) {
+  for (int t = tid; t < n * TR_C; t += TR_T) {
     int i = t % n, c = t / n;
     int src = unit ? perm[i] : i;
-    X[i + c * n] = B[src + (c0 + c) * (long long)n];
+    X[i + c * n] = c < nc ? B[src + (c0 + c) * (long long)n] : 0.0;
   }
   __syncthreads();
+  const int ri = tid & 31, cc = tid >> 5;  // row in block, column (TR_C = 8 = warps)
   for (int p0 = 0; p0 < n; p0 += 32) {
-    int pw = n - p0 < 32 ? n - p0 : 32;
+    const int pw = min(32, n - p0);
     // X_p -= L[p, 0:p0] X[0:p0]
-    if (p0 > 0)
-      for (int t = tid; t < pw * nc; t += 256) {
-        int i = p0 + t % pw, c = t / pw;
-        double s = 0.0;
-        const double* xl = X + c * n;
-        for (int q = 0; q < p0; ++q) s += L[i + (long long)q * n] * xl[q];
-        X[i + c * n] -= s;
+    double acc = 0.0;
+    for (int q0 = 0; q0 < p0; q0 += 32) {
+      for (int t = tid; t < 32 * 32; t += TR_T) {
+        int i = t % 32, k = t / 32;
+        Ls[i][k] = i < pw ? L[(p0 + i) + (long long)(q0 + k) * n] : 0.0;
       }
-    __syncthreads();
-    // forward substitution inside the block, one thread per column
-    if (tid < nc) {
-      double* xc = X + tid * n;
-      for (int i = p0; i < p0 + pw; ++i) {
-        double s = xc[i];
-        for (int q = p0; q < i; ++q) s -= L[i + (long long)q * n] * xc[q];
-        xc[i] = unit ? s : s / L[i + (long long)i * n];
-      }
+      __syncthreads();
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) acc += Ls[ri][k] * X[(q0 + k) + cc * n];
+      __syncthreads();
+    }
+    // diagonal block: load L_pp, then warp cc solves column cc (lane = row)
+    for (int t = tid; t < 32 * 32; t += TR_T) {
+      int i = t % 32, k = t / 32;
+      Ls[i][k] = (i < pw && k < pw) ? L[(p0 + i) + (long long)(p0 + k) * n] : 0.0;
     }
     __syncthreads();
+    double xi = ri < pw ? X[(p0 + ri) + cc * n] - acc : 0.0;
+    for (int j = 0; j < pw; ++j) {
+      double xj = __shfl_sync(0xffffffffu, xi, j);
+      if (!unit) xj /= Ls[j][j];
+      if (lane == j) xi = xj;
+      if (lane > j) xi -= Ls[lane][j] * xj;
+    }
+    if (ri < pw) X[(p0 + ri) + cc * n] = xi;
+    __syncthreads();
+    (void)warp;
   }
   if (unit && d) {
     // D^{-1} (dense_kernels.cpp:126-144)
@@ -416,7 +443,7 @@ __global__ void __launch_bounds__(256) trsm_panel_kernel(const double* L, int n,
     }
     __syncthreads();
   }
-  for (int t = tid; t < n * nc; t += 256) {
+  for (int t = tid; t < n * nc; t += TR_T) {
     int i = t % n, c = t / n;
     B[i + (c0 + c) * (long long)n] = X[i + c * n];
   }
@@ -430,7 +457,7 @@ void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* pe
   static size_t lim = enable_max_dyn_smem(trsm_panel_kernel);
   if (bytes > lim) throw CudaError("trsm_panel: tile too large for shared memory");
   unsigned blocks = (unsigned)((nrhs + TR_C - 1) / TR_C);
-  trsm_panel_kernel<<<blocks, 256, bytes, st>>>(L, n, B, nrhs, perm, d, e, s2, info);
+  trsm_panel_kernel<<<blocks, TR_T, bytes, st>>>(L, n, B, nrhs, perm, d, e, s2, info);
   TLRG_CUDA(cudaGetLastError());
 }
 

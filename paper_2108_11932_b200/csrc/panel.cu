@@ -1,0 +1,363 @@
+// Per-tile latency kernels of an ARA round:
+//   * rng_draw  : tlr::Rng gaussian blocks.  Warp 0 walks the mt19937_64
+//                 stream and the polar accept/reject decisions (integer work,
+//                 one ballot per 32 attempts); all warps then evaluate
+//                 sqrt(-2 log s / s) for the accepted pairs in parallel.
+//   * panel_tau : tau = 100 * eps_mach * ||Y_raw||_F (dense_kernels.cpp:391-392)
+//   * panel_mgs : one sweep of the reference's panel MGS2 with deficiency
+//                 replacement (dense_kernels.cpp:331-375) + R <- Rp R and the
+//                 finalisation of orthog (dense_kernels.cpp:397-417).
+//                 Every thread owns a fixed set of rows, so the only
+//                 synchronisations are the three block reductions per column
+//                 (two re-orthogonalisation passes + the norm).
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace tlrg {
+
+// ------------------------------------------------------------------ RNG ---
+__global__ void rng_seed_kernel(RngState* states, const uint64_t* seeds, int n) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) rng_seed(&states[t], seeds[t]);
+}
+
+constexpr int RT = 128;      // threads per draw CTA
+constexpr int RCH = 1024;    // accepted pairs staged per chunk
+
+__global__ void __launch_bounds__(RT) rng_draw_kernel(RngState* states, const int* idx,
+                                                      double* out, long long count,
+                                                      long long out_stride) {
+  __shared__ uint64_t mt[MT_N];
+  __shared__ double pu[RCH], pv[RCH], ps[RCH];
+  __shared__ int s_idx, s_hc, s_target;
+  __shared__ double s_c;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  RngState* g = &states[idx ? idx[blockIdx.x] : blockIdx.x];
+  double* o = out + (long long)blockIdx.x * out_stride;
+  for (int i = tid; i < MT_N; i += RT) mt[i] = g->mt[i];
+  if (tid == 0) {
+    s_idx = g->idx;
+    s_hc = g->have_cached;
+    s_c = g->cached;
+  }
+  __syncthreads();
+  long long produced = 0;
+  if (s_hc && count > 0) {
+    if (tid == 0) o[0] = s_c;
+    produced = 1;
+    __syncthreads();
+    if (tid == 0) s_hc = 0;
+  }
+  while (produced < count) {
+    const long long need = count - produced;
+    const long long need_att = (need + 1) / 2;
+    if (warp == 0) {
+      int target = (int)(need_att < RCH ? need_att : RCH);
+      int got = 0, ix = s_idx;
+      while (got < target) {
+        if (ix >= MT_N) {
+          warp_mt_twist(mt);
+          ix = 0;
+        }
+        int n_att = (MT_N - ix) / 2;
+        if (n_att > 32) n_att = 32;
+        bool acc = false;
+        double u = 0, v = 0, s = 0;
+        if (lane < n_att) {
+          u = 2.0 * mt_uniform(mt_temper(mt[ix + 2 * lane])) - 1.0;
+          v = 2.0 * mt_uniform(mt_temper(mt[ix + 2 * lane + 1])) - 1.0;
+          s = u * u + v * v;
+          acc = (s < 1.0) && (s != 0.0);
+        }
+        unsigned mask = __ballot_sync(0xffffffffu, acc);
+        int rank = __popc(mask & ((1u << lane) - 1u));
+        int nacc = __popc(mask), left = target - got;
+        if (acc && rank < left) {
+          pu[got + rank] = u;
+          pv[got + rank] = v;
+          ps[got + rank] = s;
+        }
+        if (nacc >= left) {
+          unsigned m2 = mask;
+          for (int t = 0; t < left - 1; ++t) m2 &= m2 - 1;
+          ix += 2 * (__ffs(m2) - 1 + 1);
+          got = target;
+        } else {
+          ix += 2 * n_att;
+          got += nacc;
+        }
+      }
+      if (lane == 0) {
+        s_idx = ix;
+        s_target = target;
+      }
+    }
+    __syncthreads();
+    const int target = s_target;
+    for (int i = tid; i < target; i += RT) {
+      double s = ps[i];
+      double f = sqrt(-2.0 * log(s) / s);
+      long long p0 = produced + 2LL * i;
+      o[p0] = pu[i] * f;
+      if (p0 + 1 < count) {
+        o[p0 + 1] = pv[i] * f;
+      } else {
+        s_hc = 1;  // odd tail: cache the second value (util.hpp:43-45)
+        s_c = pv[i] * f;
+      }
+    }
+    produced += 2LL * target;
+    __syncthreads();
+  }
+  for (int i = tid; i < MT_N; i += RT) g->mt[i] = mt[i];
+  if (tid == 0) {
+    g->idx = s_idx;
+    g->have_cached = s_hc;
+    g->cached = s_c;
+  }
+}
+
+void rng_seed(RngState* states, const uint64_t* d_seeds, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  rng_seed_kernel<<<(n + 127) / 128, 128, 0, st>>>(states, d_seeds, n);
+  TLRG_CUDA(cudaGetLastError());
+}
+void rng_draw(RngState* states, const int* d_idx, int ntiles, double* out, long long count,
+              long long out_stride, cudaStream_t st) {
+  if (ntiles <= 0 || count <= 0) return;
+  rng_draw_kernel<<<ntiles, RT, 0, st>>>(states, d_idx, out, count, out_stride);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------- PANEL TAU ---
+__global__ void __launch_bounds__(256) panel_tau_kernel(PanelTask* tasks) {
+  __shared__ double red[32];
+  PanelTask& T = tasks[blockIdx.x];
+  long long n = (long long)T.rows * T.width;
+  double s = 0.0;
+  for (long long e = threadIdx.x; e < n; e += 256) s += T.Y[e] * T.Y[e];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    double tau = 100.0 * DBL_EPSILON * sqrt(s);
+    T.tau = tau == 0.0 ? DBL_MIN : tau;
+  }
+}
+void panel_tau(PanelTask* d_tasks, int ntask, cudaStream_t st) {
+  if (ntask <= 0) return;
+  panel_tau_kernel<<<ntask, 256, 0, st>>>(d_tasks);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------- PANEL MGS ---
+constexpr int PT = 128;
+constexpr int PW = PT / 32;
+
+struct PanelSmem {
+  double* part;  // [2][PW][part_len]
+  double* cbuf;  // [max(part_len, rows)]
+  int cbuf_len;  // = part_len (stride of the partial buffers)
+  int buf;
+};
+
+// Block-reduce `nv` per-thread partial values (already warp-summed into lane 0)
+// -> cbuf[0..nv).  One __syncthreads.
+__device__ __forceinline__ void reduce_to(PanelSmem& S, int nv) {
+  __syncthreads();
+  double* P = S.part + (size_t)S.buf * PW * S.cbuf_len;
+  for (int p = threadIdx.x; p < nv; p += PT) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < PW; ++w) s += P[w * S.cbuf_len + p];
+    S.cbuf[p] = s;
+  }
+  S.buf ^= 1;
+  __syncthreads();
+}
+
+// one classical re-orthogonalisation pass of column j against columns < j;
+// coefficients are returned in S.cbuf
+__device__ __forceinline__ void cgs_pass(double* Y, int rows, int j, PanelSmem& S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* yj = Y + (long long)j * rows;
+  double* P = S.part + (size_t)S.buf * PW * S.cbuf_len + warp * S.cbuf_len;
+#pragma unroll 4
+  for (int p = 0; p < j; ++p) {
+    const double* yp = Y + (long long)p * rows;
+    double s = 0.0;
+    for (int r = threadIdx.x; r < rows; r += PT) s += yp[r] * yj[r];
+    s = warp_sum(s);
+    if (lane == 0) P[p] = s;
+  }
+  reduce_to(S, j);
+  double* yw = Y + (long long)j * rows;
+  for (int r = threadIdx.x; r < rows; r += PT) {
+    double s = 0.0;
+    for (int p = 0; p < j; ++p) s += S.cbuf[p] * Y[(long long)p * rows + r];
+    yw[r] -= s;
+  }
+}
+
+__device__ __forceinline__ double col_norm(const double* y, int rows, PanelSmem& S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double s = 0.0;
+  for (int r = threadIdx.x; r < rows; r += PT) s += y[r] * y[r];
+  s = warp_sum(s);
+  if (lane == 0) S.part[(size_t)S.buf * PW * S.cbuf_len + warp * S.cbuf_len] = s;
+  reduce_to(S, 1);
+  return sqrt(S.cbuf[0]);
+}
+
+__global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int sweep, int finalize,
+                                                       int ys_in_smem, int rp_in_smem,
+                                                       int part_len, int cbuf_len) {
+  extern __shared__ double smem[];
+  PanelSmem S;
+  S.part = smem;
+  S.cbuf = S.part + 2 * PW * part_len;
+  S.cbuf_len = part_len;
+  S.buf = 0;
+  uint64_t* smt = reinterpret_cast<uint64_t*>(S.cbuf + cbuf_len);
+  double* dyn = reinterpret_cast<double*>(smt + MT_N);
+
+  PanelTask& T = tasks[blockIdx.x];
+  const int rows = T.rows, w = T.width, q = T.q;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* Rp = rp_in_smem ? dyn : T.Rp;
+  double* Y = ys_in_smem ? dyn + (rp_in_smem ? (size_t)w * w : 0) : T.Y;
+  if (ys_in_smem)
+    for (long long e = tid; e < (long long)rows * w; e += PT) Y[e] = T.Y[e];
+  for (long long e = tid; e < (long long)w * w; e += PT) Rp[e] = 0.0;
+  if (sweep == 0)
+    for (int j = tid; j < w; j += PT) {
+      T.deficient[j] = 0;
+      T.tiny[j] = 0.0;
+    }
+  __shared__ int rng_loaded, s_idx, s_hc;
+  __shared__ double s_c;
+  if (tid == 0) rng_loaded = 0;
+  __syncthreads();
+  const double tau = T.tau;
+
+  for (int j = 0; j < w; ++j) {
+    double* yj = Y + (long long)j * rows;
+    if (j > 0)
+      for (int pass = 0; pass < 2; ++pass) {
+        cgs_pass(Y, rows, j, S);
+        if (tid == 0)
+          for (int p = 0; p < j; ++p) Rp[p + (long long)j * w] += S.cbuf[p];
+      }
+    double nj = col_norm(yj, rows, S);
+    if (!(nj >= tau)) {
+      // deficient column: record, restart from a fresh direction of the tile's
+      // own stream, project out Q and the earlier panel columns
+      if (tid == 0 && !T.deficient[j]) {
+        T.deficient[j] = 1;
+        T.tiny[j] = isfinite(nj) ? nj : 0.0;
+      }
+      if (warp == 0) {
+        int ix, hc;
+        double c;
+        if (!rng_loaded) {
+          warp_rng_load(T.rng, smt, ix, hc, c);
+        } else {
+          ix = s_idx;
+          hc = s_hc;
+          c = s_c;
+        }
+        warp_rng_draw(smt, ix, hc, c, yj, rows);
+        if (lane == 0) {
+          s_idx = ix;
+          s_hc = hc;
+          s_c = c;
+          rng_loaded = 1;
+        }
+      }
+      __syncthreads();
+      if (q > 0) {
+        for (int t = warp; t < q; t += PW) {
+          const double* qt = T.Q + (long long)t * rows;
+          double s = 0.0;
+          for (int r = lane; r < rows; r += 32) s += qt[r] * yj[r];
+          s = warp_sum(s);
+          if (lane == 0) S.cbuf[t] = s;
+        }
+        __syncthreads();
+        for (int r = tid; r < rows; r += PT) {
+          double s = 0.0;
+          for (int t = 0; t < q; ++t) s += T.Q[(long long)t * rows + r] * S.cbuf[t];
+          yj[r] -= s;
+        }
+        __syncthreads();
+      }
+      if (j > 0)
+        for (int pass = 0; pass < 2; ++pass) cgs_pass(Y, rows, j, S);
+      nj = col_norm(yj, rows, S);
+      if (nj == 0.0) {
+        // pathological: unit coordinate direction, written by the row's owner
+        if (tid == (j % rows) % PT) yj[j % rows] = 1.0;
+        nj = 1.0;
+      }
+      if (tid == 0) Rp[j + (long long)j * w] = 0.0;
+    } else {
+      if (tid == 0) Rp[j + (long long)j * w] = nj;
+    }
+    const double inv = 1.0 / nj;
+    for (int r = tid; r < rows; r += PT) yj[r] *= inv;
+  }
+  __syncthreads();
+  if (rng_loaded && warp == 0) warp_rng_store(T.rng, smt, s_idx, s_hc, s_c);
+  if (ys_in_smem)
+    for (long long e = tid; e < (long long)rows * w; e += PT) T.Y[e] = Y[e];
+
+  // R <- Rp * R  (R = I before the first sweep)
+  double* R = T.R;
+  if (sweep == 0) {
+    for (long long e = tid; e < (long long)w * w; e += PT) R[e] = Rp[e];
+  } else {
+    double* Rt = T.Rp + (long long)w * w;
+    for (long long e = tid; e < (long long)w * w; e += PT) {
+      int p = (int)(e % w), jj = (int)(e / w);
+      double s = 0.0;
+      for (int t = p; t <= jj; ++t) s += Rp[p + (long long)t * w] * R[t + (long long)jj * w];
+      Rt[e] = p <= jj ? s : 0.0;
+    }
+    __syncthreads();
+    for (long long e = tid; e < (long long)w * w; e += PT) R[e] = Rt[e];
+  }
+  __syncthreads();
+  if (finalize) {
+    for (int jj = tid; jj < w; jj += PT) {
+      if (T.deficient[jj]) {
+        for (int i = 0; i < w; ++i) R[i + (long long)jj * w] = 0.0;
+        R[jj + (long long)jj * w] = T.tiny[jj];
+        T.col_norms[jj] = T.tiny[jj];
+        T.new_mass[jj] = T.tiny[jj];
+      } else {
+        double s = 0.0;
+        for (int i = 0; i <= jj; ++i) s += R[i + (long long)jj * w] * R[i + (long long)jj * w];
+        T.col_norms[jj] = sqrt(s);
+        T.new_mass[jj] = fabs(R[jj + (long long)jj * w]);
+      }
+    }
+  }
+}
+
+void panel_mgs(PanelTask* d_tasks, int ntask, int sweep, int finalize, int max_width,
+               int max_rows, cudaStream_t st) {
+  if (ntask <= 0) return;
+  int part_len = max_width;
+  int cbuf_len = max_width > max_rows ? max_width : max_rows;
+  size_t base = ((size_t)2 * PW * part_len + cbuf_len + MT_N) * 8;
+  static size_t lim = enable_max_dyn_smem(panel_mgs_kernel);
+  size_t rp = (size_t)max_width * max_width * 8;
+  size_t ys = (size_t)max_rows * max_width * 8;
+  int rp_in = base + rp <= lim;
+  int ys_in = base + (rp_in ? rp : 0) + ys <= lim;
+  size_t bytes = base + (rp_in ? rp : 0) + (ys_in ? ys : 0);
+  panel_mgs_kernel<<<ntask, PT, bytes, st>>>(d_tasks, sweep, finalize, ys_in, rp_in, part_len,
+                                             cbuf_len);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+}  // namespace tlrg
