@@ -175,6 +175,8 @@ int tlrg_gemm(tlrg_ctx ctx, int32_t M, int32_t N, int32_t K, int32_t transA, int
 
 /* Library version string and the sm target it was built for. */
 const char* tlrg_version(void);
+/* cudaProfilerStart/Stop, to scope ncu / nsys captures to a region */
+void tlrg_profiler(int on);
 
 #ifdef __cplusplus
 }

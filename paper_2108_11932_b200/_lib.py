@@ -52,6 +52,7 @@ class StatusC(C.Structure):
 # exported symbol -> (restype, argtypes); this table is also the export check
 SIGNATURES = {
     "tlrg_version": (C.c_char_p, []),
+    "tlrg_profiler": (None, [C.c_int]),
     "tlrg_default_ara_config": (None, [C.POINTER(AraConfigC)]),
     "tlrg_default_workspace": (None, [C.POINTER(WorkspaceC)]),
     "tlrg_default_factor_options": (None, [C.POINTER(FactorOptionsC)]),

@@ -73,10 +73,49 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   int* ints = C.buf<int>("ints", (size_t)T * 6);
   int *qcols = ints, *rounds = ints + T, *conv = ints + 2 * T, *done = ints + 3 * T,
       *rcount = ints + 4 * T, *rpos = ints + 5 * T;
-  RngState* rng = C.buf<RngState>("rng", (size_t)T);
   TLRG_CUDA(cudaMemsetAsync(ints, 0, sizeof(int) * T * 6, C.st));
-  rng_seed(rng, C.push(S.seeds), T, C.st);
+  // per-tile gaussian streams (exact tlr::Rng sequences), consumed by cursor
+  GaussStreams G;
+  G.st = C.buf<RngState>("rng", (size_t)T);
+  G.cap = 6LL * cols * bs + 4LL * bs * maxrows;
+  G.buf = C.buf<double>("gbuf", (size_t)T * G.cap);
+  long long* gl = C.buf<long long>("gcur", (size_t)2 * T);
+  G.avail = gl;
+  G.cursor = gl + T;
+  TLRG_CUDA(cudaMemsetAsync(gl, 0, sizeof(long long) * 2 * T, C.st));
+  rng_seed(G.st, C.push(S.seeds), T, C.st);
   ++C.launches;
+  std::vector<long long> h_av(T, 0), h_cur(T, 0);
+  const long long gchunk = 2LL * cols * bs;
+  // make sure every listed slot has `need` values ready beyond its cursor
+  auto ensure = [&](const std::vector<int>& slots, const std::vector<long long>& need) {
+    std::vector<int> gen, cmp;
+    std::vector<long long> want;
+    for (size_t t = 0; t < slots.size(); ++t) {
+      int s = slots[t];
+      if (h_av[s] - h_cur[s] >= need[t]) continue;
+      if (G.cap - h_cur[s] < need[t] + gchunk) {
+        cmp.push_back(s);
+        h_av[s] -= h_cur[s];
+        h_cur[s] = 0;
+      }
+      long long w = std::min(G.cap, h_cur[s] + need[t] + gchunk);
+      w = (w + 1) & ~1LL;
+      if (w > G.cap) w = G.cap & ~1LL;
+      gen.push_back(s);
+      want.push_back(w);
+      h_av[s] = w;
+    }
+    if (!cmp.empty()) {
+      gauss_compact(G, C.push(cmp), (int)cmp.size(), C.st);
+      ++C.launches;
+    }
+    if (!gen.empty()) {
+      gauss_generate(G, C.push(gen), C.push(want), (int)gen.size(), C.st);
+      ++C.launches;
+    }
+  };
+  long long* h_gcur = nullptr;
 
   std::vector<int> q(T, 0);
   std::vector<int> act(T);
@@ -86,7 +125,12 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   while (!act.empty()) {
     const int Ta = (int)act.size();
     tm.start(C.st);
-    rng_draw(rng, C.push(act), Ta, Om, (long long)cols * bs, (long long)cols * bs, C.st);
+    {
+      std::vector<long long> need(Ta);
+      for (int t = 0; t < Ta; ++t) need[t] = (long long)cols * bs + 2LL * bs * S.rows[act[t]];
+      ensure(act, need);
+    }
+    gauss_gather(G, C.push(act), Ta, Om, (long long)cols * bs, (long long)cols * bs, C.st);
     ++C.launches;
     op.sample(act, Om, Y, Ystride);
     tm.stop(C.st);
@@ -104,7 +148,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       P.deficient = defi + (size_t)s * bs;
       P.col_norms = cn + (size_t)s * bs;
       P.new_mass = nm + (size_t)s * bs;
-      P.rng = rng + s;
+      P.gbuf = G.buf + (long long)s * G.cap;
+      P.gcursor = G.cursor + s;
       P.rows = S.rows[s];
       P.width = bs;
       P.q = q[s];
@@ -165,7 +210,11 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     to.stop(C.st);
     TLRG_CUDA(cudaMemcpyAsync(h_flags, done, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
     TLRG_CUDA(cudaMemcpyAsync(h_flags + T, qcols, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
+    if (!h_gcur) h_gcur = reinterpret_cast<long long*>(C.pinned_dbl((size_t)T));
+    TLRG_CUDA(cudaMemcpyAsync(h_gcur, G.cursor, sizeof(long long) * T, cudaMemcpyDeviceToHost,
+                              C.st));
     C.sync();
+    for (int s = 0; s < T; ++s) h_cur[s] = h_gcur[s];
     cst.t_sampling += tm.sec();
     cst.t_orthog += to.sec();
     cst.tile_rounds += Ta;
@@ -222,6 +271,16 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     std::vector<PanelTask> tasks;
     std::vector<SvdTask> svd;
     std::vector<int> sl;
+    {
+      std::vector<int> need_s;
+      std::vector<long long> need;
+      for (int s = 0; s < T; ++s)
+        if (q[s]) {
+          need_s.push_back(s);
+          need.push_back(2LL * q[s] * cols);  // every column replaced in both sweeps
+        }
+      ensure(need_s, need);
+    }
     for (int s = 0; s < T; ++s) {
       if (q[s] == 0) continue;
       PanelTask P{};
@@ -233,7 +292,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       P.col_norms = P.tiny + qmax;
       P.new_mass = P.tiny + 2 * qmax;
       P.deficient = df + (size_t)s * qmax;
-      P.rng = rng + s;
+      P.gbuf = G.buf + (long long)s * G.cap;
+      P.gcursor = G.cursor + s;
       P.rows = cols;
       P.width = q[s];
       P.q = 0;

@@ -1,4 +1,6 @@
 // extern "C" boundary (include/tlrg.h) over the device implementation.
+#include <cuda_profiler_api.h>
+
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
@@ -210,6 +212,11 @@ void upload_d(DUpload& u, const Matrix& M, const double* dd, const double* de, c
 extern "C" {
 
 const char* tlrg_version(void) { return "tlrg 0.1 (sm_100a, FP64 DMMA)"; }
+
+void tlrg_profiler(int on) {
+  if (on) cudaProfilerStart();
+  else cudaProfilerStop();
+}
 
 void tlrg_default_ara_config(tlrg_ara_config* c) {
   c->block_samples = 32;
@@ -697,12 +704,21 @@ void tlrg_ara_free(tlrg_ara a) { delete a; }
 int tlrg_rng_gaussians(tlrg_ctx ctx, uint64_t seed, int64_t n, double* out, tlrg_status* st) {
   return guarded(st, [&] {
     Ctx& C = ctx->c;
-    RngState* rs = C.buf<RngState>("t_rng", 1);
-    double* d = C.buf<double>("t_rng_out", (size_t)n + 1);
+    // through the stream generator used by the factorization
+    GaussStreams G;
+    G.cap = (n + 2) & ~1LL;
+    G.st = C.buf<RngState>("t_rng", 1);
+    G.buf = C.buf<double>("t_rng_out", (size_t)G.cap + 2);
+    long long* gl = C.buf<long long>("t_rng_cur", 2);
+    G.avail = gl;
+    G.cursor = gl + 1;
+    TLRG_CUDA(cudaMemsetAsync(gl, 0, sizeof(long long) * 2, C.st));
     std::vector<uint64_t> s1{seed};
-    rng_seed(rs, C.push(s1), 1, C.st);
-    rng_draw(rs, nullptr, 1, d, n, n, C.st);
-    TLRG_CUDA(cudaMemcpyAsync(out, d, 8 * n, cudaMemcpyDeviceToHost, C.st));
+    rng_seed(G.st, C.push(s1), 1, C.st);
+    std::vector<int> slot{0};
+    std::vector<long long> want{G.cap};
+    gauss_generate(G, C.push(slot), C.push(want), 1, C.st);
+    TLRG_CUDA(cudaMemcpyAsync(out, G.buf, 8 * n, cudaMemcpyDeviceToHost, C.st));
     C.sync();
   });
 }
@@ -720,16 +736,27 @@ int tlrg_orthog(tlrg_ctx ctx, const double* Q, int32_t rows, int32_t q, double* 
     double* dRp = C.buf<double>("o_Rp", (size_t)2 * k * k);
     double* vec = C.buf<double>("o_vec", (size_t)4 * k);
     uint8_t* df = C.buf<uint8_t>("o_df", (size_t)k);
-    RngState* rs = C.buf<RngState>("o_rng", 1);
+    GaussStreams G;
+    G.cap = 2LL * k * rows + 4;
+    G.st = C.buf<RngState>("o_rng", 1);
+    G.buf = C.buf<double>("o_gbuf", (size_t)G.cap);
+    long long* gl = C.buf<long long>("o_gcur", 2);
+    G.avail = gl;
+    G.cursor = gl + 1;
+    TLRG_CUDA(cudaMemsetAsync(gl, 0, sizeof(long long) * 2, C.st));
+    std::vector<uint64_t> s1{seed};
+    rng_seed(G.st, C.push(s1), 1, C.st);
+    std::vector<int> slot{0};
+    std::vector<long long> want{G.cap};
+    gauss_generate(G, C.push(slot), C.push(want), 1, C.st);
     if (q) TLRG_CUDA(cudaMemcpyAsync(dQ, Q, 8 * (size_t)rows * q, cudaMemcpyHostToDevice, C.st));
     TLRG_CUDA(cudaMemcpyAsync(dY, Y, 8 * (size_t)rows * k, cudaMemcpyHostToDevice, C.st));
-    std::vector<uint64_t> s1{seed};
-    rng_seed(rs, C.push(s1), 1, C.st);
     std::vector<PanelTask> t(1);
     PanelTask& P = t[0];
     P = PanelTask{};
     P.Y = dY; P.Q = q ? dQ : nullptr; P.R = dR; P.Rp = dRp; P.tiny = vec;
-    P.col_norms = vec + k; P.new_mass = vec + 2 * k; P.deficient = df; P.rng = rs;
+    P.col_norms = vec + k; P.new_mass = vec + 2 * k; P.deficient = df;
+    P.gbuf = G.buf; P.gcursor = G.cursor;
     P.rows = rows; P.width = k; P.q = q;
     PanelTask* d = C.push(t);
     panel_tau(d, 1, C.st);
@@ -743,16 +770,14 @@ int tlrg_orthog(tlrg_ctx ctx, const double* Q, int32_t rows, int32_t q, double* 
       }
       panel_mgs(d, 1, sweep, sweep == 1, k, rows, C.st);
     }
+    long long cur = 0;
     TLRG_CUDA(cudaMemcpyAsync(Y, dY, 8 * (size_t)rows * k, cudaMemcpyDeviceToHost, C.st));
     TLRG_CUDA(cudaMemcpyAsync(R, dR, 8 * (size_t)k * k, cudaMemcpyDeviceToHost, C.st));
     TLRG_CUDA(cudaMemcpyAsync(col_norms, vec + k, 8 * k, cudaMemcpyDeviceToHost, C.st));
     TLRG_CUDA(cudaMemcpyAsync(new_mass, vec + 2 * k, 8 * k, cudaMemcpyDeviceToHost, C.st));
-    if (next_draw) {
-      double* nd = C.buf<double>("o_nd", 2);
-      rng_draw(rs, nullptr, 1, nd, 1, 1, C.st);
-      TLRG_CUDA(cudaMemcpyAsync(next_draw, nd, 8, cudaMemcpyDeviceToHost, C.st));
-    }
+    TLRG_CUDA(cudaMemcpyAsync(&cur, G.cursor, 8, cudaMemcpyDeviceToHost, C.st));
     C.sync();
+    if (next_draw) TLRG_CUDA(cudaMemcpy(next_draw, G.buf + cur, 8, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -188,11 +188,12 @@ void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint
     double* work = C.buf<double>("sc_work", (size_t)2 * p * p);
     double* sig = C.buf<double>("sc_sig", (size_t)p);
     int* rk = C.buf<int>("sc_rank", 1);
-    RngState* rs = C.buf<RngState>("sc_rng", 1);
-    {
-      std::vector<uint64_t> s1{mix64(seed ^ 0x5c1ULL)};
-      rng_seed(rs, C.push(s1), 1, C.st);
-    }
+    // replacement directions for rank-deficient sketch columns (not part of the
+    // reference's streams): a counter-based gaussian pool consumed by cursor
+    double* pool = C.buf<double>("sc_pool", (size_t)4 * n * p);
+    long long* pcur = C.buf<long long>("sc_pcur", 1);
+    TLRG_CUDA(cudaMemsetAsync(pcur, 0, sizeof(long long), C.st));
+    fill_gaussian_philox(pool, 4LL * n * p, mix64(seed ^ 0x5c1ULL) + attempt, C.st);
     fill_gaussian_philox(Om, (long long)n * p, seed * 0x9E3779B97F4A7C15ULL + attempt, C.st);
     auto DtimesX = [&](const double* X, double* out) {
       std::vector<GemmProblem> pr(1);
@@ -206,7 +207,8 @@ void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint
       PanelTask& P = t[0];
       P = PanelTask{};
       P.Y = X; P.Q = nullptr; P.R = R; P.Rp = Rp; P.tiny = vec; P.col_norms = vec + p;
-      P.new_mass = vec + 2 * p; P.deficient = df; P.rng = rs; P.rows = n; P.width = p; P.q = 0;
+      P.new_mass = vec + 2 * p; P.deficient = df; P.gbuf = pool; P.gcursor = pcur;
+      P.rows = n; P.width = p; P.q = 0;
       PanelTask* d = C.push(t);
       panel_tau(d, 1, C.st);
       panel_mgs(d, 1, 0, 0, p, n, C.st);

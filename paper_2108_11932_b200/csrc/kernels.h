@@ -35,6 +35,25 @@ void rng_seed(RngState* states, const uint64_t* d_seeds, int n, cudaStream_t st)
 void rng_draw(RngState* states, const int* d_state_idx, int ntiles, double* out,
               long long count, long long out_stride, cudaStream_t st);
 
+// Per-tile Gaussian streams (pre-generated, consumed by cursor).  The stream of
+// slot s is the exact tlr::Rng(seed_s).gaussian() sequence; generation always
+// appends whole polar pairs, so no pair cache is needed.
+struct GaussStreams {
+  RngState* st = nullptr;     // generator state, positioned after avail[s] values
+  double* buf = nullptr;      // slot s at buf + s*cap
+  long long cap = 0;
+  long long* avail = nullptr;   // device, values generated
+  long long* cursor = nullptr;  // device, values consumed
+};
+// append values to the listed slots until avail >= want (want is rounded up to even)
+void gauss_generate(const GaussStreams& G, const int* d_slots, const long long* d_want, int n,
+                    cudaStream_t st);
+// out + a*out_stride <- next `count` values of slot d_slots[a]; advances cursors
+void gauss_gather(const GaussStreams& G, const int* d_slots, int n, double* out, long long count,
+                  long long out_stride, cudaStream_t st);
+// move [cursor, avail) to the front of each listed slot
+void gauss_compact(const GaussStreams& G, const int* d_slots, int n, cudaStream_t st);
+
 // --------------------------------------------------------------- ORTHOG ---
 // One panel of the reference's orthog (dense_kernels.cpp:331-420) per task.
 struct PanelTask {
@@ -46,7 +65,8 @@ struct PanelTask {
   uint8_t* deficient; // width
   double* col_norms;  // width (written when finalize)
   double* new_mass;   // width
-  RngState* rng;
+  const double* gbuf; // tile's gaussian stream (deficient-column replacements)
+  long long* gcursor; // its cursor (device)
   double tau;         // 100 * DBL_EPSILON * ||Y_raw||_F (or DBL_MIN)
   int rows, width, q;
 };

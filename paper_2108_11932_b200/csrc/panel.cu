@@ -130,6 +130,134 @@ void rng_draw(RngState* states, const int* d_idx, int ntiles, double* out, long 
   TLRG_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------ STREAMS ----
+__global__ void __launch_bounds__(RT) gauss_generate_kernel(GaussStreams G, const int* slots,
+                                                            const long long* want) {
+  __shared__ uint64_t mt[MT_N];
+  __shared__ double pu[RCH], pv[RCH], ps[RCH];
+  __shared__ int s_idx, s_target;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s = slots[blockIdx.x];
+  long long have = G.avail[s];
+  long long target = want[blockIdx.x];
+  if (target > G.cap) target = G.cap;
+  target &= ~1LL;
+  if (have >= target) return;
+  RngState* g = &G.st[s];
+  double* buf = G.buf + (long long)s * G.cap;
+  for (int i = tid; i < MT_N; i += RT) mt[i] = g->mt[i];
+  if (tid == 0) s_idx = g->idx;
+  __syncthreads();
+  while (have < target) {
+    const long long need_pairs = (target - have) / 2;
+    if (warp == 0) {
+      int chunk = (int)(need_pairs < RCH ? need_pairs : RCH);
+      int got = 0, ix = s_idx;
+      while (got < chunk) {
+        if (ix >= MT_N) {
+          warp_mt_twist(mt);
+          ix = 0;
+        }
+        int n_att = (MT_N - ix) / 2;
+        if (n_att > 32) n_att = 32;
+        bool acc = false;
+        double u = 0, v = 0, q = 0;
+        if (lane < n_att) {
+          u = 2.0 * mt_uniform(mt_temper(mt[ix + 2 * lane])) - 1.0;
+          v = 2.0 * mt_uniform(mt_temper(mt[ix + 2 * lane + 1])) - 1.0;
+          q = u * u + v * v;
+          acc = (q < 1.0) && (q != 0.0);
+        }
+        unsigned mask = __ballot_sync(0xffffffffu, acc);
+        int rank = __popc(mask & ((1u << lane) - 1u));
+        int nacc = __popc(mask), left = chunk - got;
+        if (acc && rank < left) {
+          pu[got + rank] = u;
+          pv[got + rank] = v;
+          ps[got + rank] = q;
+        }
+        if (nacc >= left) {
+          unsigned m2 = mask;
+          for (int t = 0; t < left - 1; ++t) m2 &= m2 - 1;
+          ix += 2 * __ffs(m2);
+          got = chunk;
+        } else {
+          ix += 2 * n_att;
+          got += nacc;
+        }
+      }
+      if (lane == 0) {
+        s_idx = ix;
+        s_target = chunk;
+      }
+    }
+    __syncthreads();
+    const int chunk = s_target;
+    for (int i = tid; i < chunk; i += RT) {
+      double q = ps[i];
+      double f = sqrt(-2.0 * log(q) / q);
+      buf[have + 2 * i] = pu[i] * f;
+      buf[have + 2 * i + 1] = pv[i] * f;
+    }
+    have += 2LL * chunk;
+    __syncthreads();
+  }
+  for (int i = tid; i < MT_N; i += RT) g->mt[i] = mt[i];
+  if (tid == 0) {
+    g->idx = s_idx;
+    g->have_cached = 0;
+    G.avail[s] = have;
+  }
+}
+
+__global__ void __launch_bounds__(256) gauss_gather_kernel(GaussStreams G, const int* slots,
+                                                           double* out, long long count,
+                                                           long long out_stride) {
+  const int s = slots[blockIdx.x];
+  const long long c0 = G.cursor[s];
+  const double* src = G.buf + (long long)s * G.cap + c0;
+  double* dst = out + (long long)blockIdx.x * out_stride;
+  for (long long e = threadIdx.x; e < count; e += 256) dst[e] = src[e];
+  __syncthreads();
+  if (threadIdx.x == 0) G.cursor[s] = c0 + count;
+}
+
+__global__ void __launch_bounds__(256) gauss_compact_kernel(GaussStreams G, const int* slots) {
+  const int s = slots[blockIdx.x];
+  const long long c0 = G.cursor[s], a = G.avail[s];
+  double* b = G.buf + (long long)s * G.cap;
+  // forward copy is safe: destination index < source index
+  for (long long base = 0; base < a - c0; base += 256) {
+    long long e = base + threadIdx.x;
+    double v = e < a - c0 ? b[c0 + e] : 0.0;
+    __syncthreads();
+    if (e < a - c0) b[e] = v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    G.cursor[s] = 0;
+    G.avail[s] = a - c0;
+  }
+}
+
+void gauss_generate(const GaussStreams& G, const int* d_slots, const long long* d_want, int n,
+                    cudaStream_t st) {
+  if (n <= 0) return;
+  gauss_generate_kernel<<<n, RT, 0, st>>>(G, d_slots, d_want);
+  TLRG_CUDA(cudaGetLastError());
+}
+void gauss_gather(const GaussStreams& G, const int* d_slots, int n, double* out, long long count,
+                  long long out_stride, cudaStream_t st) {
+  if (n <= 0 || count <= 0) return;
+  gauss_gather_kernel<<<n, 256, 0, st>>>(G, d_slots, out, count, out_stride);
+  TLRG_CUDA(cudaGetLastError());
+}
+void gauss_compact(const GaussStreams& G, const int* d_slots, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  gauss_compact_kernel<<<n, 256, 0, st>>>(G, d_slots);
+  TLRG_CUDA(cudaGetLastError());
+}
+
 // ------------------------------------------------------------- PANEL TAU ---
 __global__ void __launch_bounds__(256) panel_tau_kernel(PanelTask* tasks) {
   __shared__ double red[32];
@@ -180,16 +308,33 @@ __device__ __forceinline__ void reduce_to(PanelSmem& S, int nv) {
 __device__ __forceinline__ void cgs_pass(double* Y, int rows, int j, PanelSmem& S) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* yj = Y + (long long)j * rows;
-  double* P = S.part + (size_t)S.buf * PW * S.cbuf_len + warp * S.cbuf_len;
-#pragma unroll 4
-  for (int p = 0; p < j; ++p) {
-    const double* yp = Y + (long long)p * rows;
-    double s = 0.0;
-    for (int r = threadIdx.x; r < rows; r += PT) s += yp[r] * yj[r];
-    s = warp_sum(s);
-    if (lane == 0) P[p] = s;
+  // warps split the coefficients; each dot runs over all rows (one warp sum)
+  __syncthreads();  // y_j (and cbuf readers of the previous pass) are settled
+  int p = warp;
+  for (; p + PW < j; p += 2 * PW) {
+    const double* ya = Y + (long long)p * rows;
+    const double* yb = Y + (long long)(p + PW) * rows;
+    double sa = 0.0, sb = 0.0;
+    for (int r = lane; r < rows; r += 32) {
+      double y = yj[r];
+      sa += ya[r] * y;
+      sb += yb[r] * y;
+    }
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane == 0) {
+      S.cbuf[p] = sa;
+      S.cbuf[p + PW] = sb;
+    }
   }
-  reduce_to(S, j);
+  if (p < j) {
+    const double* ya = Y + (long long)p * rows;
+    double sa = 0.0;
+    for (int r = lane; r < rows; r += 32) sa += ya[r] * yj[r];
+    sa = warp_sum(sa);
+    if (lane == 0) S.cbuf[p] = sa;
+  }
+  __syncthreads();
   double* yw = Y + (long long)j * rows;
   for (int r = threadIdx.x; r < rows; r += PT) {
     double s = 0.0;
@@ -233,9 +378,6 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
       T.deficient[j] = 0;
       T.tiny[j] = 0.0;
     }
-  __shared__ int rng_loaded, s_idx, s_hc;
-  __shared__ double s_c;
-  if (tid == 0) rng_loaded = 0;
   __syncthreads();
   const double tau = T.tau;
 
@@ -255,23 +397,12 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
         T.deficient[j] = 1;
         T.tiny[j] = isfinite(nj) ? nj : 0.0;
       }
-      if (warp == 0) {
-        int ix, hc;
-        double c;
-        if (!rng_loaded) {
-          warp_rng_load(T.rng, smt, ix, hc, c);
-        } else {
-          ix = s_idx;
-          hc = s_hc;
-          c = s_c;
-        }
-        warp_rng_draw(smt, ix, hc, c, yj, rows);
-        if (lane == 0) {
-          s_idx = ix;
-          s_hc = hc;
-          s_c = c;
-          rng_loaded = 1;
-        }
+      {
+        // the next `rows` values of the tile's stream (dense_kernels.cpp:351)
+        const long long c0 = *T.gcursor;
+        __syncthreads();
+        for (int r = tid; r < rows; r += PT) yj[r] = T.gbuf[c0 + r];
+        if (tid == 0) *T.gcursor = c0 + rows;
       }
       __syncthreads();
       if (q > 0) {
@@ -306,7 +437,6 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
     for (int r = tid; r < rows; r += PT) yj[r] *= inv;
   }
   __syncthreads();
-  if (rng_loaded && warp == 0) warp_rng_store(T.rng, smt, s_idx, s_hc, s_c);
   if (ys_in_smem)
     for (long long e = tid; e < (long long)rows * w; e += PT) T.Y[e] = Y[e];
 

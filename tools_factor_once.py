@@ -8,5 +8,8 @@ cfgname = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 kind, n, b, eps, bs, kern, ell, nug, mode = bench.CONFIGS[cfgname]
 A = build_tlr(bench.problem_points(cfgname), kern, ell, nug, b, eps,
               cfg=tg.AraConfig(block_samples=bs, seed=12345))
+ctx = A.ctx
+ctx.lib.tlrg_profiler(1)
 F = (tg.tlr_cholesky if mode == 0 else tg.tlr_ldlt)(A, tg.AraConfig(block_samples=bs, eps=eps, seed=12345))
+ctx.lib.tlrg_profiler(0)
 print("t_device", F.stats.t_device, "launches", F.stats.kernel_launches)
