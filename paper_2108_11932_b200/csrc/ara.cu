@@ -40,6 +40,14 @@ struct Timer {
     cudaEventDestroy(b);
   }
 };
+__global__ void ara_loop_cond_kernel(cudaGraphConditionalHandle h, int* active, int max_rounds) {
+  int it = ++active[1];
+  cudaGraphSetConditional(h, (active[0] > 0 && it < max_rounds) ? 1 : 0);
+}
+void ara_loop_cond(cudaGraphConditionalHandle h, int* active, int max_rounds, cudaStream_t st) {
+  ara_loop_cond_kernel<<<1, 1, 0, st>>>(h, active, max_rounds);
+  TLRG_CUDA(cudaGetLastError());
+}
 }  // namespace
 
 void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,
@@ -115,121 +123,132 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       ++C.launches;
     }
   };
-  long long* h_gcur = nullptr;
+  int h_flags_unused = 0;
 
   std::vector<int> q(T, 0);
-  std::vector<int> act(T);
-  std::iota(act.begin(), act.end(), 0);
-  int* h_flags = C.pinned_ints((size_t)2 * T);
-  Timer tm, to;
-  while (!act.empty()) {
-    const int Ta = (int)act.size();
-    tm.start(C.st);
-    {
-      std::vector<long long> need(Ta);
-      for (int t = 0; t < Ta; ++t) need[t] = (long long)cols * bs + 2LL * bs * S.rows[act[t]];
-      ensure(act, need);
-    }
-    gauss_gather(G, C.push(act), Ta, Om, (long long)cols * bs, (long long)cols * bs, C.st);
-    ++C.launches;
-    op.sample(act, Om, Y, Ystride);
-    tm.stop(C.st);
-    to.start(C.st);
-    std::vector<PanelTask> tasks(Ta);
-    for (int a = 0; a < Ta; ++a) {
-      int s = act[a];
-      PanelTask& P = tasks[a];
-      P = PanelTask{};
-      P.Y = Y + s * Ystride;
-      P.Q = Q + s * Qstride;
-      P.R = R + (size_t)s * bs * bs;
-      P.Rp = Rp + (size_t)s * 2 * bs * bs;
-      P.tiny = tiny + (size_t)s * bs;
-      P.deficient = defi + (size_t)s * bs;
-      P.col_norms = cn + (size_t)s * bs;
-      P.new_mass = nm + (size_t)s * bs;
-      P.gbuf = G.buf + (long long)s * G.cap;
-      P.gcursor = G.cursor + s;
-      P.rows = S.rows[s];
-      P.width = bs;
-      P.q = q[s];
-    }
-    PanelTask* d_tasks = C.push(tasks);
-    panel_tau(d_tasks, Ta, C.st);
-    ++C.launches;
-    for (int sweep = 0; sweep < 2; ++sweep) {
-      // Y <- Y - Q (Q^T Y)  (dense_kernels.cpp:398-401)
-      std::vector<GemmProblem> p1, p2;
-      for (int a = 0; a < Ta; ++a) {
-        int s = act[a];
-        if (q[s] == 0) continue;
-        GemmProblem g{};
-        g.A = Q + s * Qstride; g.lda = S.rows[s]; g.transA = 1;
-        g.B = Y + s * Ystride; g.ldb = S.rows[s];
-        g.C = Cdef + (size_t)s * capmax * bs; g.ldc = q[s];
-        g.M = q[s]; g.N = bs; g.K = S.rows[s]; g.alpha = 1.0;
-        p1.push_back(g);
-        GemmProblem h{};
-        h.A = Q + s * Qstride; h.lda = S.rows[s];
-        h.B = Cdef + (size_t)s * capmax * bs; h.ldb = q[s];
-        h.C = Y + s * Ystride; h.ldc = S.rows[s];
-        h.M = S.rows[s]; h.N = bs; h.K = q[s]; h.alpha = -1.0; h.beta = 1.0;
-        p2.push_back(h);
-      }
-      if (!p1.empty()) {
-        C.gemm(p1);
-        C.gemm(p2);
-      }
-      panel_mgs(d_tasks, Ta, sweep, sweep == 1, bs, maxrows, C.st);
-      ++C.launches;
-    }
-    std::vector<AbsorbTask> ab(Ta);
-    for (int a = 0; a < Ta; ++a) {
-      int s = act[a];
-      AbsorbTask& A = ab[a];
-      A.Y = Y + s * Ystride;
-      A.Q = Q + s * Qstride;
-      A.col_norms = cn + (size_t)s * bs;
-      A.new_mass = nm + (size_t)s * bs;
-      A.recent = recent + (size_t)s * window;
-      A.qcols = qcols + s;
-      A.recent_count = rcount + s;
-      A.recent_pos = rpos + s;
-      A.rounds = rounds + s;
-      A.converged = conv + s;
-      A.done = done + s;
-      A.rows = S.rows[s];
-      A.bs = bs;
-      A.cap = S.cap[s];
-      A.window = window;
-      A.eps = cfg.eps;
-      A.eta = cfg.safety;
-    }
-    ara_absorb(C.push(ab), Ta, C.st);
-    ++C.launches;
-    to.stop(C.st);
-    TLRG_CUDA(cudaMemcpyAsync(h_flags, done, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
-    TLRG_CUDA(cudaMemcpyAsync(h_flags + T, qcols, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
-    if (!h_gcur) h_gcur = reinterpret_cast<long long*>(C.pinned_dbl((size_t)T));
-    TLRG_CUDA(cudaMemcpyAsync(h_gcur, G.cursor, sizeof(long long) * T, cudaMemcpyDeviceToHost,
+  int* active = C.buf<int>("active", 2);  // [0] tiles still resident, [1] loop counter
+  int* d_rows = C.buf<int>("slot_rows", (size_t)T);
+  {
+    std::vector<int> init{T, 0};
+    TLRG_CUDA(cudaMemcpyAsync(active, init.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, C.st));
+    TLRG_CUDA(cudaMemcpyAsync(d_rows, S.rows.data(), sizeof(int) * T, cudaMemcpyHostToDevice,
                               C.st));
-    C.sync();
-    for (int s = 0; s < T; ++s) h_cur[s] = h_gcur[s];
-    cst.t_sampling += tm.sec();
-    cst.t_orthog += to.sec();
-    cst.tile_rounds += Ta;
-    for (int a = 0; a < Ta; ++a)
-      if (!S.Sref.empty()) cst.flops_ref += bs * S.Sref[act[a]];
-    std::vector<int> stay;
-    for (int s : act) {
-      q[s] = h_flags[T + s];
-      if (!h_flags[s]) stay.push_back(s);
-    }
-    act.swap(stay);
   }
-  std::vector<int> h_rounds(T), h_conv(T);
-  TLRG_CUDA(cudaMemcpy(h_rounds.data(), rounds, sizeof(int) * T, cudaMemcpyDeviceToHost));
-  TLRG_CUDA(cudaMemcpy(h_conv.data(), conv, sizeof(int) * T, cudaMemcpyDeviceToHost));
+  // ---- static per-column launch tables (staged before capture) ---------------
+  std::vector<std::vector<GemmProblem>> stages;
+  op.sample_plan(Om, Y, Ystride, done, stages);
+  std::vector<GemmPlan> sample_plans;
+  for (auto& st : stages) sample_plans.push_back(gemm_plan(st, C.desc, C.st));
+  std::vector<GemmProblem> pc, py;
+  for (int s = 0; s < T; ++s) {
+    GemmProblem g{};
+    g.A = Q + s * Qstride; g.lda = S.rows[s]; g.transA = 1;
+    g.B = Y + s * Ystride; g.ldb = S.rows[s];
+    g.C = Cdef + (size_t)s * capmax * bs; g.ldc = S.cap[s];
+    g.M = S.cap[s]; g.N = bs; g.K = S.rows[s]; g.alpha = 1.0;
+    g.Mp = qcols + s; g.skip = done + s;
+    pc.push_back(g);
+    GemmProblem h{};
+    h.A = Q + s * Qstride; h.lda = S.rows[s];
+    h.B = Cdef + (size_t)s * capmax * bs; h.ldb = S.cap[s];
+    h.C = Y + s * Ystride; h.ldc = S.rows[s];
+    h.M = S.rows[s]; h.N = bs; h.K = S.cap[s]; h.alpha = -1.0; h.beta = 1.0;
+    h.Kp = qcols + s; h.skip = done + s;
+    py.push_back(h);
+  }
+  GemmPlan plan_c = gemm_plan(pc, C.desc, C.st), plan_y = gemm_plan(py, C.desc, C.st);
+  std::vector<PanelTask> tasks(T);
+  for (int s = 0; s < T; ++s) {
+    PanelTask& P = tasks[s];
+    P = PanelTask{};
+    P.Y = Y + s * Ystride;
+    P.Q = Q + s * Qstride;
+    P.R = R + (size_t)s * bs * bs;
+    P.Rp = Rp + (size_t)s * 2 * bs * bs;
+    P.tiny = tiny + (size_t)s * bs;
+    P.deficient = defi + (size_t)s * bs;
+    P.col_norms = cn + (size_t)s * bs;
+    P.new_mass = nm + (size_t)s * bs;
+    P.gbuf = G.buf + (long long)s * G.cap;
+    P.gcursor = G.cursor + s;
+    P.rows = S.rows[s];
+    P.width = bs;
+    P.done = done + s;
+    P.qdev = qcols + s;
+    P.Qw = Q + s * Qstride;
+    P.recent = recent + (size_t)s * window;
+    P.qcols = qcols + s;
+    P.rcount = rcount + s;
+    P.rpos = rpos + s;
+    P.rounds = rounds + s;
+    P.conv = conv + s;
+    P.donew = done + s;
+    P.active = active;
+    P.cap = S.cap[s];
+    P.window = window;
+    P.eps = cfg.eps;
+    P.eta = cfg.safety;
+  }
+  PanelTask* d_tasks = C.push(tasks);
+  int capall = 0;
+  for (int s = 0; s < T; ++s) capall = std::max(capall, S.cap[s]);
+  const int max_rounds = 4 * capall + 8;  // a tile gains >= 1 column per round or converges
+
+  // ---- the round loop: one CUDA graph, conditional WHILE node on device ------
+  Timer tm;
+  tm.start(C.st);
+  cudaGraph_t graph = nullptr, body = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  TLRG_CUDA(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle handle;
+  TLRG_CUDA(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  TLRG_CUDA(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+  body = cp.conditional.phGraph_out[0];
+  TLRG_CUDA(cudaStreamBeginCaptureToGraph(C.st, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed));
+  gauss_round(G, done, d_rows, T, cols, bs, Om, C.st);
+  for (auto& pl : sample_plans) gemm_launch(pl, C.st);
+  panel_tau(d_tasks, T, C.st);
+  for (int sweep = 0; sweep < 2; ++sweep) {
+    gemm_launch(plan_c, C.st);  // C = Q^T Y      (dense_kernels.cpp:399)
+    gemm_launch(plan_y, C.st);  // Y -= Q C       (dense_kernels.cpp:400)
+    panel_mgs(d_tasks, T, sweep, sweep == 1, bs, maxrows, C.st);
+  }
+  ara_loop_cond(handle, active, max_rounds, C.st);
+  TLRG_CUDA(cudaStreamEndCapture(C.st, &body));
+  TLRG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  TLRG_CUDA(cudaGraphLaunch(exec, C.st));
+  tm.stop(C.st);
+  std::vector<int> hq(T), h_rounds(T), h_conv(T), hact(2);
+  std::vector<long long> hav(T), hcur(T);
+  TLRG_CUDA(cudaMemcpyAsync(hq.data(), qcols, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
+  TLRG_CUDA(cudaMemcpyAsync(h_rounds.data(), rounds, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
+  TLRG_CUDA(cudaMemcpyAsync(h_conv.data(), conv, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
+  TLRG_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * 2, cudaMemcpyDeviceToHost, C.st));
+  TLRG_CUDA(cudaMemcpyAsync(hav.data(), G.avail, sizeof(long long) * T, cudaMemcpyDeviceToHost,
+                            C.st));
+  TLRG_CUDA(cudaMemcpyAsync(hcur.data(), G.cursor, sizeof(long long) * T, cudaMemcpyDeviceToHost,
+                            C.st));
+  C.sync();
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  if (hact[0] > 0) throw CudaError("ara_batch: round limit reached with tiles still resident");
+  C.launches += (long long)hact[1] * (4 + (long long)sample_plans.size() + 6);
+  cst.t_sampling += tm.sec();  // the fused round loop (draws, sampling, orthog, absorb)
+  for (int s = 0; s < T; ++s) {
+    q[s] = hq[s];
+    h_av[s] = hav[s];
+    h_cur[s] = hcur[s];
+    cst.tile_rounds += h_rounds[s];
+    if (!S.Sref.empty()) cst.flops_ref += (double)bs * h_rounds[s] * S.Sref[s];
+  }
+  (void)h_flags_unused;
 
   // ---- exit projection B = E^T Q (ara.cpp:380-387), all tiles at once ------
   Timer tp, tr;

@@ -153,18 +153,17 @@ std::unique_ptr<Matrix> build_tlr_device(Ctx& C, int dim, int64_t n, const doubl
       sl.seeds.push_back(tile_seed(cfg.seed, 0xb11dULL, i, j));
     }
     AraOperator op;
-    op.sample = [&](const std::vector<int>& act, const double* Om, double* Y, long long Ys) {
-      std::vector<GemmProblem> pr;
-      for (size_t a = 0; a < act.size(); ++a) {
-        int s = act[a];
+    op.sample_plan = [&](const double* Om, double* Y, long long Ys, const int* done,
+                         std::vector<std::vector<GemmProblem>>& stages) {
+      stages.assign(1, {});
+      for (int s = 0; s < T; ++s) {
         GemmProblem g{};
         g.A = D + (size_t)s * b * b; g.lda = sl.rows[s];
-        g.B = Om + a * (size_t)b * cfg.bs; g.ldb = b;
+        g.B = Om + (size_t)s * b * cfg.bs; g.ldb = b;
         g.C = Y + s * Ys; g.ldc = sl.rows[s];
-        g.M = sl.rows[s]; g.N = cfg.bs; g.K = b; g.alpha = 1.0;
-        pr.push_back(g);
+        g.M = sl.rows[s]; g.N = cfg.bs; g.K = b; g.alpha = 1.0; g.skip = done + s;
+        stages[0].push_back(g);
       }
-      C.gemm(pr);
     };
     op.project = [&](const std::vector<int>& q, const double* Q, long long Qs, double* Bb,
                      const std::vector<long long>& boff) {

@@ -210,52 +210,42 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
   double* T1 = K ? C.buf<double>("T1", (size_t)K * bs * T) : nullptr;
 
   AraOperator op;
-  // Y_s = U^A (V^A^T Omega) - H_s (U_k,:^T Omega)   (Eq. 1 with the j-sum in H)
-  op.sample = [&](const std::vector<int>& act, const double* Om, double* Y, long long Ystride) {
-    const int Ta = (int)act.size();
-    std::vector<GemmProblem> pr;
-    if (K > 0) {
-      GemmProblem g{};
-      g.A = cs.Ucat; g.lda = rk; g.transA = 1;
-      g.B = Om; g.ldb = rk;
-      g.C = T1; g.ldc = K;
-      g.M = K; g.N = Ta * bs; g.K = rk; g.alpha = 1.0;
-      pr.push_back(g);
-    }
-    for (int a = 0; a < Ta; ++a) {
-      int s = act[a];
-      if (kA[s] == 0) continue;
-      GemmProblem g{};
-      g.A = M.V[M.t(queue[s], k)]; g.lda = rk; g.transA = 1;
-      g.B = Om + (size_t)a * rk * bs; g.ldb = rk;
-      g.C = Z + (size_t)s * kAmax * bs; g.ldc = kA[s];
-      g.M = kA[s]; g.N = bs; g.K = rk; g.alpha = 1.0;
-      pr.push_back(g);
-    }
-    C.gemm(pr);
-    pr.clear();
-    for (int a = 0; a < Ta; ++a) {
-      int s = act[a];
-      GemmProblem g{};
-      g.A = kA[s] ? M.U[M.t(queue[s], k)] : Y; g.lda = S.rows[s];
-      g.B = kA[s] ? Z + (size_t)s * kAmax * bs : Y; g.ldb = std::max(kA[s], 1);
-      g.C = Y + s * Ystride; g.ldc = S.rows[s];
-      g.M = S.rows[s]; g.N = bs; g.K = kA[s]; g.alpha = 1.0; g.beta = 0.0;
-      pr.push_back(g);
-    }
-    C.gemm(pr);
-    if (K > 0) {
-      pr.clear();
-      for (int a = 0; a < Ta; ++a) {
-        int s = act[a];
+  // Y_s = U^A (V^A^T Omega_s) - H_s (U_k,:^T Omega_s)   (Eq. 1 with the j-sum in H)
+  op.sample_plan = [&](const double* Om, double* Y, long long Ystride, const int* done,
+                       std::vector<std::vector<GemmProblem>>& stages) {
+    stages.assign(3, {});
+    for (int s = 0; s < T; ++s) {
+      const double* Oms = Om + (size_t)s * rk * bs;
+      if (K > 0) {
         GemmProblem g{};
-        g.A = H + s * Hstride; g.lda = S.rows[s];
-        g.B = T1 + (size_t)a * bs * K; g.ldb = K;
-        g.C = Y + s * Ystride; g.ldc = S.rows[s];
-        g.M = S.rows[s]; g.N = bs; g.K = K; g.alpha = -1.0; g.beta = 1.0;
-        pr.push_back(g);
+        g.A = cs.Ucat; g.lda = rk; g.transA = 1;
+        g.B = Oms; g.ldb = rk;
+        g.C = T1 + (size_t)s * bs * K; g.ldc = K;
+        g.M = K; g.N = bs; g.K = rk; g.alpha = 1.0; g.skip = done + s;
+        stages[0].push_back(g);
       }
-      C.gemm(pr);
+      if (kA[s] > 0) {
+        GemmProblem g{};
+        g.A = M.V[M.t(queue[s], k)]; g.lda = rk; g.transA = 1;
+        g.B = Oms; g.ldb = rk;
+        g.C = Z + (size_t)s * kAmax * bs; g.ldc = kA[s];
+        g.M = kA[s]; g.N = bs; g.K = rk; g.alpha = 1.0; g.skip = done + s;
+        stages[0].push_back(g);
+      }
+      GemmProblem y{};
+      y.A = kA[s] ? M.U[M.t(queue[s], k)] : Y; y.lda = S.rows[s];
+      y.B = kA[s] ? Z + (size_t)s * kAmax * bs : Y; y.ldb = std::max(kA[s], 1);
+      y.C = Y + s * Ystride; y.ldc = S.rows[s];
+      y.M = S.rows[s]; y.N = bs; y.K = kA[s]; y.alpha = 1.0; y.beta = 0.0; y.skip = done + s;
+      stages[1].push_back(y);
+      if (K > 0) {
+        GemmProblem h{};
+        h.A = H + s * Hstride; h.lda = S.rows[s];
+        h.B = T1 + (size_t)s * bs * K; h.ldb = K;
+        h.C = Y + s * Ystride; h.ldc = S.rows[s];
+        h.M = S.rows[s]; h.N = bs; h.K = K; h.alpha = -1.0; h.beta = 1.0; h.skip = done + s;
+        stages[2].push_back(h);
+      }
     }
   };
   // B_s = V^A (U^A^T Q) - U_k,: (H_s^T Q)

@@ -212,9 +212,11 @@ struct AraSlots {
   int cols = 0;
 };
 struct AraOperator {
-  // enqueue Y_s = E_s Omega_a for the active slots (Omega_a at Om + a*cols*bs)
-  std::function<void(const std::vector<int>& act, const double* Om, double* Y,
-                     long long Ystride)> sample;
+  // GEMM stages computing Y_s = E_s Omega_s for every slot s (Omega_s at
+  // Om + s*cols*bs, Y_s at Y + s*Ystride); each problem must carry
+  // skip = done + s so converged tiles cost nothing in later rounds
+  std::function<void(const double* Om, double* Y, long long Ystride, const int* done,
+                     std::vector<std::vector<GemmProblem>>& stages)> sample_plan;
   // enqueue B_s = E_s^T Q_s (cols x q_s, ld cols) at Bb + boff[s] for q_s > 0
   std::function<void(const std::vector<int>& q, const double* Q, long long Qstride, double* Bb,
                      const std::vector<long long>& boff)> project;

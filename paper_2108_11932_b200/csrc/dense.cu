@@ -452,9 +452,9 @@ __global__ void __launch_bounds__(TR_T) trsm_panel_kernel(const double* L, int n
 void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
                 const double* d, const double* e, const uint8_t* s2, int* info,
                 cudaStream_t st) {
+  static size_t lim = enable_max_dyn_smem(trsm_panel_kernel);
   if (nrhs <= 0 || n <= 0) return;
   size_t bytes = (size_t)n * TR_C * 8;
-  static size_t lim = enable_max_dyn_smem(trsm_panel_kernel);
   if (bytes > lim) throw CudaError("trsm_panel: tile too large for shared memory");
   unsigned blocks = (unsigned)((nrhs + TR_C - 1) / TR_C);
   trsm_panel_kernel<<<blocks, TR_T, bytes, st>>>(L, n, B, nrhs, perm, d, e, s2, info);

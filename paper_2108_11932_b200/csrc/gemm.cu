@@ -61,7 +61,7 @@ void release_retired_arenas() {
 }
 
 template <int BM, int BN>
-static void launch_grouped(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
+static GemmPlan plan_grouped(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
   std::vector<GemmProblem> live;
   live.reserve(probs.size());
   long long tiles = 0;
@@ -72,21 +72,34 @@ static void launch_grouped(std::vector<GemmProblem>& probs, DescArena& desc, cud
     tiles += (long long)((p.M + BM - 1) / BM) * p.tiles_n;
     live.push_back(p);
   }
-  if (tiles == 0) return;
+  GemmPlan plan;
+  plan.bn = BN;
+  if (tiles == 0) return plan;
   if (tiles > 0x7fffffffLL) throw std::runtime_error("grouped_gemm: too many tiles");
-  auto* d = (const GemmProblem*)desc.push(live.data(), live.size() * sizeof(GemmProblem), st);
-  grouped_gemm_kernel<BM, BN><<<(unsigned)tiles, 128, 0, st>>>(d, (int)live.size());
+  plan.d = (const GemmProblem*)desc.push(live.data(), live.size() * sizeof(GemmProblem), st);
+  plan.n = (int)live.size();
+  plan.tiles = (int)tiles;
+  return plan;
+}
+
+GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
+  int maxN = 0;
+  for (auto& p : probs)
+    if (p.M > 0) maxN = std::max(maxN, p.N);
+  return maxN <= 16 ? plan_grouped<64, 16>(probs, desc, st) : plan_grouped<64, 32>(probs, desc, st);
+}
+
+void gemm_launch(const GemmPlan& p, cudaStream_t st) {
+  if (p.tiles == 0) return;
+  if (p.bn == 16)
+    grouped_gemm_kernel<64, 16><<<(unsigned)p.tiles, 128, 0, st>>>(p.d, p.n);
+  else
+    grouped_gemm_kernel<64, 32><<<(unsigned)p.tiles, 128, 0, st>>>(p.d, p.n);
   TLRG_CUDA(cudaGetLastError());
 }
 
 void grouped_gemm(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
-  int maxN = 0;
-  for (auto& p : probs)
-    if (p.M > 0) maxN = std::max(maxN, p.N);
-  if (maxN <= 16)
-    launch_grouped<64, 16>(probs, desc, st);
-  else
-    launch_grouped<64, 32>(probs, desc, st);
+  gemm_launch(gemm_plan(probs, desc, st), st);
 }
 
 }  // namespace tlrg

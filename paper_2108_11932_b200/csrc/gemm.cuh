@@ -27,6 +27,13 @@ struct GemmProblem {
   double alpha, beta;
   int tile_start;  // exclusive prefix of CTA tiles (filled by the launcher)
   int tiles_n;     // tiles along N
+  // optional device-resident controls (read at run time; M/K above are then
+  // upper bounds used for tiling): skip the problem when *skip != 0, take the
+  // actual M / K from *Mp / *Kp.  This keeps launches static across ARA rounds
+  // so a whole round can be captured once and replayed from a device loop.
+  const int* skip;
+  const int* Mp;
+  const int* Kp;
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
@@ -68,9 +75,13 @@ __global__ void __launch_bounds__(128) grouped_gemm_kernel(const GemmProblem* __
     s_prob = lo;
   }
   __syncthreads();
-  const GemmProblem P = probs[s_prob];
+  GemmProblem P = probs[s_prob];
   const int local = blockIdx.x - P.tile_start;
   const int m0 = (local / P.tiles_n) * BM, n0 = (local % P.tiles_n) * BN;
+  if (P.skip && *P.skip) return;
+  if (P.Mp) P.M = min(P.M, *P.Mp);
+  if (P.Kp) P.K = min(P.K, *P.Kp);
+  if (m0 >= P.M) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 1) * Cfg::WM, wn = (warp & 1) * Cfg::WN;
   const int g = lane >> 2, t4 = lane & 3;

@@ -16,6 +16,13 @@ namespace tlrg {
 // after each stream synchronisation by the caller).
 struct DescArena;
 void grouped_gemm(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st);
+// Two-step form: stage the table once (before a graph capture), launch many times.
+struct GemmPlan {
+  const GemmProblem* d = nullptr;
+  int n = 0, tiles = 0, bn = 32;
+};
+GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st);
+void gemm_launch(const GemmPlan& p, cudaStream_t st);
 
 // Device scratch for kernel argument tables: pinned host staging + device
 // mirror, bump-allocated and reset by the owner after a stream sync.
@@ -53,6 +60,11 @@ void gauss_gather(const GaussStreams& G, const int* d_slots, int n, double* out,
                   long long out_stride, cudaStream_t st);
 // move [cursor, avail) to the front of each listed slot
 void gauss_compact(const GaussStreams& G, const int* d_slots, int n, cudaStream_t st);
+// one ARA round's draws for ALL slots (skipping done ones): top the stream up
+// (compacting when needed) so that this round's Omega and every possible
+// deficient-column replacement are available, then copy Omega_s to Om + s*cols*bs.
+void gauss_round(const GaussStreams& G, const int* done, const int* rows, int nslots, int cols,
+                 int bs, double* Om, cudaStream_t st);
 
 // --------------------------------------------------------------- ORTHOG ---
 // One panel of the reference's orthog (dense_kernels.cpp:331-420) per task.
@@ -69,6 +81,21 @@ struct PanelTask {
   long long* gcursor; // its cursor (device)
   double tau;         // 100 * DBL_EPSILON * ||Y_raw||_F (or DBL_MIN)
   int rows, width, q;
+  // device-driven ARA round (all optional): skip when *done, basis width from
+  // *qdev, and in the finalising sweep run the absorb step (ara.cpp:171-195)
+  const int* done;
+  const int* qdev;
+  double* Qw;          // basis to append to (rows x cap)
+  double* recent;      // window ring [window]
+  int* qcols;          // in/out basis width
+  int* rcount;
+  int* rpos;
+  int* rounds;
+  int* conv;
+  int* donew;          // done flag written by absorb
+  int* active;         // decremented when the tile leaves
+  int cap, window;
+  double eps, eta;
 };
 // tau[t] = 100*eps*||Y_t||_F  (frobenius of the raw sample)
 void panel_tau(PanelTask* d_tasks, int ntask, cudaStream_t st);

@@ -162,10 +162,10 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
 }
 
 void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m) {
+  static size_t lim = enable_max_dyn_smem(jacobi_svd_kernel);
   if (ntask <= 0) return;
   if (max_m <= 0) max_m = max_n;
   size_t bytes = ((size_t)max_m * max_n + (size_t)max_n * max_n) * 8;
-  static size_t lim = enable_max_dyn_smem(jacobi_svd_kernel);
   int staged = bytes <= lim;
   jacobi_svd_kernel<<<ntask, JT, staged ? bytes : 16, st>>>(d_tasks, staged);
   TLRG_CUDA(cudaGetLastError());

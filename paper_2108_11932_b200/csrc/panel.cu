@@ -131,31 +131,28 @@ void rng_draw(RngState* states, const int* d_idx, int ntiles, double* out, long 
 }
 
 // ------------------------------------------------------------ STREAMS ----
-__global__ void __launch_bounds__(RT) gauss_generate_kernel(GaussStreams G, const int* slots,
-                                                            const long long* want) {
-  __shared__ uint64_t mt[MT_N];
-  __shared__ double pu[RCH], pv[RCH], ps[RCH];
-  __shared__ int s_idx, s_target;
+struct GenSmem {
+  uint64_t mt[MT_N];
+  double pu[RCH], pv[RCH], ps[RCH];
+  int idx, chunk;
+};
+
+// CTA-cooperative: append values to slot s from `have` up to `target` (even).
+__device__ void cta_generate(GaussStreams& G, int s, long long have, long long target, GenSmem& S) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int s = slots[blockIdx.x];
-  long long have = G.avail[s];
-  long long target = want[blockIdx.x];
-  if (target > G.cap) target = G.cap;
-  target &= ~1LL;
-  if (have >= target) return;
   RngState* g = &G.st[s];
   double* buf = G.buf + (long long)s * G.cap;
-  for (int i = tid; i < MT_N; i += RT) mt[i] = g->mt[i];
-  if (tid == 0) s_idx = g->idx;
+  for (int i = tid; i < MT_N; i += blockDim.x) S.mt[i] = g->mt[i];
+  if (tid == 0) S.idx = g->idx;
   __syncthreads();
   while (have < target) {
     const long long need_pairs = (target - have) / 2;
     if (warp == 0) {
       int chunk = (int)(need_pairs < RCH ? need_pairs : RCH);
-      int got = 0, ix = s_idx;
+      int got = 0, ix = S.idx;
       while (got < chunk) {
         if (ix >= MT_N) {
-          warp_mt_twist(mt);
+          warp_mt_twist(S.mt);
           ix = 0;
         }
         int n_att = (MT_N - ix) / 2;
@@ -163,8 +160,8 @@ __global__ void __launch_bounds__(RT) gauss_generate_kernel(GaussStreams G, cons
         bool acc = false;
         double u = 0, v = 0, q = 0;
         if (lane < n_att) {
-          u = 2.0 * mt_uniform(mt_temper(mt[ix + 2 * lane])) - 1.0;
-          v = 2.0 * mt_uniform(mt_temper(mt[ix + 2 * lane + 1])) - 1.0;
+          u = 2.0 * mt_uniform(mt_temper(S.mt[ix + 2 * lane])) - 1.0;
+          v = 2.0 * mt_uniform(mt_temper(S.mt[ix + 2 * lane + 1])) - 1.0;
           q = u * u + v * v;
           acc = (q < 1.0) && (q != 0.0);
         }
@@ -172,9 +169,9 @@ __global__ void __launch_bounds__(RT) gauss_generate_kernel(GaussStreams G, cons
         int rank = __popc(mask & ((1u << lane) - 1u));
         int nacc = __popc(mask), left = chunk - got;
         if (acc && rank < left) {
-          pu[got + rank] = u;
-          pv[got + rank] = v;
-          ps[got + rank] = q;
+          S.pu[got + rank] = u;
+          S.pv[got + rank] = v;
+          S.ps[got + rank] = q;
         }
         if (nacc >= left) {
           unsigned m2 = mask;
@@ -187,27 +184,84 @@ __global__ void __launch_bounds__(RT) gauss_generate_kernel(GaussStreams G, cons
         }
       }
       if (lane == 0) {
-        s_idx = ix;
-        s_target = chunk;
+        S.idx = ix;
+        S.chunk = chunk;
       }
     }
     __syncthreads();
-    const int chunk = s_target;
-    for (int i = tid; i < chunk; i += RT) {
-      double q = ps[i];
+    const int chunk = S.chunk;
+    for (int i = tid; i < chunk; i += blockDim.x) {
+      double q = S.ps[i];
       double f = sqrt(-2.0 * log(q) / q);
-      buf[have + 2 * i] = pu[i] * f;
-      buf[have + 2 * i + 1] = pv[i] * f;
+      buf[have + 2 * i] = S.pu[i] * f;
+      buf[have + 2 * i + 1] = S.pv[i] * f;
     }
     have += 2LL * chunk;
     __syncthreads();
   }
-  for (int i = tid; i < MT_N; i += RT) g->mt[i] = mt[i];
+  for (int i = tid; i < MT_N; i += blockDim.x) g->mt[i] = S.mt[i];
   if (tid == 0) {
-    g->idx = s_idx;
+    g->idx = S.idx;
     g->have_cached = 0;
     G.avail[s] = have;
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(RT) gauss_generate_kernel(GaussStreams G, const int* slots,
+                                                            const long long* want) {
+  __shared__ GenSmem S;
+  const int s = slots[blockIdx.x];
+  long long have = G.avail[s];
+  long long target = want[blockIdx.x];
+  if (target > G.cap) target = G.cap;
+  target &= ~1LL;
+  if (have >= target) return;
+  cta_generate(G, s, have, target, S);
+}
+
+__global__ void __launch_bounds__(RT) gauss_round_kernel(GaussStreams G, const int* done,
+                                                         const int* rows, int cols, int bs,
+                                                         double* Om) {
+  __shared__ GenSmem S;
+  const int s = blockIdx.x;
+  if (done[s]) return;
+  const long long need = (long long)cols * bs + 2LL * bs * rows[s];
+  const long long chunk = 2LL * cols * bs;
+  long long cur = G.cursor[s], av = G.avail[s];
+  double* b = G.buf + (long long)s * G.cap;
+  if (av - cur < need) {
+    if (G.cap - cur < need + chunk && cur > 0) {
+      // compact [cur, av) to the front (forward copy, destination below source)
+      for (long long base = 0; base < av - cur; base += RT) {
+        long long e = base + threadIdx.x;
+        double v = e < av - cur ? b[cur + e] : 0.0;
+        __syncthreads();
+        if (e < av - cur) b[e] = v;
+        __syncthreads();
+      }
+      av -= cur;
+      cur = 0;
+      if (threadIdx.x == 0) G.cursor[s] = 0;
+    }
+    long long target = cur + need + chunk;
+    if (target > G.cap) target = G.cap;
+    target = (target + 1) & ~1LL;
+    if (target > G.cap) target -= 2;
+    cta_generate(G, s, av, target, S);
+  }
+  const double* src = b + cur;
+  double* dst = Om + (long long)s * cols * bs;
+  for (long long e = threadIdx.x; e < (long long)cols * bs; e += RT) dst[e] = src[e];
+  __syncthreads();
+  if (threadIdx.x == 0) G.cursor[s] = cur + (long long)cols * bs;
+}
+
+void gauss_round(const GaussStreams& G, const int* done, const int* rows, int nslots, int cols,
+                 int bs, double* Om, cudaStream_t st) {
+  if (nslots <= 0) return;
+  gauss_round_kernel<<<nslots, RT, 0, st>>>(G, done, rows, cols, bs, Om);
+  TLRG_CUDA(cudaGetLastError());
 }
 
 __global__ void __launch_bounds__(256) gauss_gather_kernel(GaussStreams G, const int* slots,
@@ -262,6 +316,7 @@ void gauss_compact(const GaussStreams& G, const int* d_slots, int n, cudaStream_
 __global__ void __launch_bounds__(256) panel_tau_kernel(PanelTask* tasks) {
   __shared__ double red[32];
   PanelTask& T = tasks[blockIdx.x];
+  if (T.done && *T.done) return;
   long long n = (long long)T.rows * T.width;
   double s = 0.0;
   for (long long e = threadIdx.x; e < n; e += 256) s += T.Y[e] * T.Y[e];
@@ -366,7 +421,8 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
   double* dyn = reinterpret_cast<double*>(smt + MT_N);
 
   PanelTask& T = tasks[blockIdx.x];
-  const int rows = T.rows, w = T.width, q = T.q;
+  if (T.done && *T.done) return;
+  const int rows = T.rows, w = T.width, q = T.qdev ? *T.qdev : T.q;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* Rp = rp_in_smem ? dyn : T.Rp;
   double* Y = ys_in_smem ? dyn + (rp_in_smem ? (size_t)w * w : 0) : T.Y;
@@ -437,7 +493,7 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
     for (int r = tid; r < rows; r += PT) yj[r] *= inv;
   }
   __syncthreads();
-  if (ys_in_smem)
+  if (ys_in_smem && !(finalize && T.qcols))
     for (long long e = tid; e < (long long)rows * w; e += PT) T.Y[e] = Y[e];
 
   // R <- Rp * R  (R = I before the first sweep)
@@ -470,16 +526,54 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
         T.new_mass[jj] = fabs(R[jj + (long long)jj * w]);
       }
     }
+    if (T.qcols) {
+      // absorb (ara.cpp:171-195): window of post-deflation norms, keep filter,
+      // basis append, convergence / done flags
+      __shared__ int keep[64];
+      __shared__ int s_nkeep, s_q0;
+      __syncthreads();
+      if (tid == 0) {
+        int qc = *T.qcols;
+        *T.rounds += 1;
+        int cnt = *T.rcount, pos = *T.rpos;
+        for (int j = 0; j < w; ++j) {
+          T.recent[pos] = T.col_norms[j];
+          pos = (pos + 1) % T.window;
+          if (cnt < T.window) ++cnt;
+        }
+        *T.rcount = cnt;
+        *T.rpos = pos;
+        int room = T.cap - qc, nk = 0;
+        for (int j = 0; j < w && nk < room && nk < 64; ++j)
+          if (T.new_mass[j] * T.eta > T.eps) keep[nk++] = j;
+        double e = 0.0;
+        for (int t = 0; t < cnt; ++t) e = fmax(e, T.recent[t]);
+        int conv = e * T.eta <= T.eps;
+        *T.conv = conv;
+        *T.qcols = qc + nk;
+        int dn = conv || (qc + nk) >= T.cap;
+        *T.donew = dn;
+        if (dn) atomicSub(T.active, 1);
+        s_nkeep = nk;
+        s_q0 = qc;
+      }
+      __syncthreads();
+      const int nk = s_nkeep, q0 = s_q0;
+      for (long long e = tid; e < (long long)nk * rows; e += PT) {
+        int c = (int)(e / rows), r = (int)(e % rows);
+        T.Qw[(long long)(q0 + c) * rows + r] = Y[(long long)keep[c] * rows + r];
+      }
+    }
   }
 }
 
 void panel_mgs(PanelTask* d_tasks, int ntask, int sweep, int finalize, int max_width,
                int max_rows, cudaStream_t st) {
+  static size_t lim = enable_max_dyn_smem(panel_mgs_kernel);
   if (ntask <= 0) return;
   int part_len = max_width;
   int cbuf_len = max_width > max_rows ? max_width : max_rows;
   size_t base = ((size_t)2 * PW * part_len + cbuf_len + MT_N) * 8;
-  static size_t lim = enable_max_dyn_smem(panel_mgs_kernel);
   size_t rp = (size_t)max_width * max_width * 8;
   size_t ys = (size_t)max_rows * max_width * 8;
   int rp_in = base + rp <= lim;
