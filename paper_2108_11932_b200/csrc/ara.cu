@@ -14,6 +14,7 @@
 // + one-sided Jacobi SVD of R, cut at (1 - 1/eta) eps) in batches, and the
 // final factors are written into a contiguous panel.
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "core.h"
@@ -44,14 +45,51 @@ __global__ void ara_loop_cond_kernel(cudaGraphConditionalHandle h, int* active, 
   int it = ++active[1];
   cudaGraphSetConditional(h, (active[0] > 0 && it < max_rounds) ? 1 : 0);
 }
+__global__ void ara_loop_count_kernel(int* active) { ++active[1]; }
+void ara_loop_cond_host(int* active, cudaStream_t st) {
+  ara_loop_count_kernel<<<1, 1, 0, st>>>(active);
+  TLRG_CUDA(cudaGetLastError());
+}
 void ara_loop_cond(cudaGraphConditionalHandle h, int* active, int max_rounds, cudaStream_t st) {
   ara_loop_cond_kernel<<<1, 1, 0, st>>>(h, active, max_rounds);
   TLRG_CUDA(cudaGetLastError());
 }
 }  // namespace
 
+void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int bs, int maxrows,
+                     int rounds_ahead, StreamPrep& P) {
+  const int T = (int)seeds.size();
+  P.T = T;
+  P.seeds = seeds;
+  GaussStreams& G = P.G;
+  G.st = C.buf<RngState>("p_rng", (size_t)T);
+  G.cap = 6LL * cols * bs + 4LL * bs * maxrows;
+  G.buf = C.buf<double>("p_gbuf", (size_t)T * G.cap);
+  long long* gl = C.buf<long long>("p_gcur", (size_t)2 * T);
+  G.avail = gl;
+  G.cursor = gl + T;
+  P.pre = std::min<long long>(G.cap, (long long)rounds_ahead * cols * bs + 2LL * bs * maxrows);
+  P.pre &= ~1LL;
+  uint64_t* d_seeds = C.buf<uint64_t>("p_seeds", (size_t)T);
+  int* d_slots = C.buf<int>("p_slots", (size_t)T);
+  long long* d_want = C.buf<long long>("p_want", (size_t)T);
+  std::vector<int> slots(T);
+  std::vector<long long> want(T, P.pre);
+  for (int s = 0; s < T; ++s) slots[s] = s;
+  TLRG_CUDA(cudaMemsetAsync(gl, 0, sizeof(long long) * 2 * T, C.st2));
+  TLRG_CUDA(cudaMemcpyAsync(d_seeds, seeds.data(), 8 * T, cudaMemcpyHostToDevice, C.st2));
+  TLRG_CUDA(cudaMemcpyAsync(d_slots, slots.data(), 4 * T, cudaMemcpyHostToDevice, C.st2));
+  TLRG_CUDA(cudaMemcpyAsync(d_want, want.data(), 8 * T, cudaMemcpyHostToDevice, C.st2));
+  rng_seed(G.st, d_seeds, T, C.st2);
+  gauss_generate(G, d_slots, d_want, T, C.st2);
+  C.launches += 2;
+  if (!P.ev) TLRG_CUDA(cudaEventCreateWithFlags(&P.ev, cudaEventDisableTiming));
+  TLRG_CUDA(cudaEventRecord(P.ev, C.st2));
+}
+
 void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,
-               const std::vector<int>& out_order, ColumnStats& cst, AraOut& out) {
+               const std::vector<int>& out_order, ColumnStats& cst, AraOut& out,
+               StreamPrep* pre) {
   const int T = (int)S.rows.size();
   const int bs = cfg.bs, cols = S.cols;
   const int window = cfg.window > 0 ? cfg.window : bs;
@@ -84,16 +122,23 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   TLRG_CUDA(cudaMemsetAsync(ints, 0, sizeof(int) * T * 6, C.st));
   // per-tile gaussian streams (exact tlr::Rng sequences), consumed by cursor
   GaussStreams G;
-  G.st = C.buf<RngState>("rng", (size_t)T);
-  G.cap = 6LL * cols * bs + 4LL * bs * maxrows;
-  G.buf = C.buf<double>("gbuf", (size_t)T * G.cap);
-  long long* gl = C.buf<long long>("gcur", (size_t)2 * T);
-  G.avail = gl;
-  G.cursor = gl + T;
-  TLRG_CUDA(cudaMemsetAsync(gl, 0, sizeof(long long) * 2 * T, C.st));
-  rng_seed(G.st, C.push(S.seeds), T, C.st);
-  ++C.launches;
   std::vector<long long> h_av(T, 0), h_cur(T, 0);
+  if (pre && pre->T == T && pre->seeds == S.seeds &&
+      pre->G.cap >= 6LL * cols * bs + 4LL * bs * maxrows) {
+    G = pre->G;
+    TLRG_CUDA(cudaStreamWaitEvent(C.st, pre->ev, 0));
+    for (int s = 0; s < T; ++s) h_av[s] = pre->pre;
+  } else {
+    G.st = C.buf<RngState>("rng", (size_t)T);
+    G.cap = 6LL * cols * bs + 4LL * bs * maxrows;
+    G.buf = C.buf<double>("gbuf", (size_t)T * G.cap);
+    long long* gl = C.buf<long long>("gcur", (size_t)2 * T);
+    G.avail = gl;
+    G.cursor = gl + T;
+    TLRG_CUDA(cudaMemsetAsync(gl, 0, sizeof(long long) * 2 * T, C.st));
+    rng_seed(G.st, C.push(S.seeds), T, C.st);
+    ++C.launches;
+  }
   const long long gchunk = 2LL * cols * bs;
   // make sure every listed slot has `need` values ready beyond its cursor
   auto ensure = [&](const std::vector<int>& slots, const std::vector<long long>& need) {
@@ -157,6 +202,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     py.push_back(h);
   }
   GemmPlan plan_c = gemm_plan(pc, C.desc, C.st), plan_y = gemm_plan(py, C.desc, C.st);
+  double* rep = C.buf<double>("rep", (size_t)T * maxrows * bs);
+  double* repC = C.buf<double>("repC", (size_t)T * capmax * bs);
   std::vector<PanelTask> tasks(T);
   for (int s = 0; s < T; ++s) {
     PanelTask& P = tasks[s];
@@ -171,6 +218,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     P.new_mass = nm + (size_t)s * bs;
     P.gbuf = G.buf + (long long)s * G.cap;
     P.gcursor = G.cursor + s;
+    P.rep = rep + (size_t)s * maxrows * bs;
+    P.repC = repC + (size_t)s * capmax * bs;
     P.rows = S.rows[s];
     P.width = bs;
     P.done = done + s;
@@ -197,33 +246,51 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   // ---- the round loop: one CUDA graph, conditional WHILE node on device ------
   Timer tm;
   tm.start(C.st);
-  cudaGraph_t graph = nullptr, body = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  TLRG_CUDA(cudaGraphCreate(&graph, 0));
-  cudaGraphConditionalHandle handle;
-  TLRG_CUDA(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = handle;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t cnode;
-  TLRG_CUDA(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
-  body = cp.conditional.phGraph_out[0];
-  TLRG_CUDA(cudaStreamBeginCaptureToGraph(C.st, body, nullptr, nullptr, 0,
-                                          cudaStreamCaptureModeRelaxed));
-  gauss_round(G, done, d_rows, T, cols, bs, Om, C.st);
-  for (auto& pl : sample_plans) gemm_launch(pl, C.st);
-  panel_tau(d_tasks, T, C.st);
-  for (int sweep = 0; sweep < 2; ++sweep) {
-    gemm_launch(plan_c, C.st);  // C = Q^T Y      (dense_kernels.cpp:399)
-    gemm_launch(plan_y, C.st);  // Y -= Q C       (dense_kernels.cpp:400)
-    panel_mgs(d_tasks, T, sweep, sweep == 1, bs, maxrows, C.st);
+  std::vector<std::pair<cudaGraphExec_t, cudaGraph_t>> graph_cleanup;
+  auto enqueue_round = [&]() {
+    gauss_round(G, done, d_rows, T, cols, bs, Om, C.st);
+    for (auto& pl : sample_plans) gemm_launch(pl, C.st);
+    panel_tau(d_tasks, T, C.st);
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      gemm_launch(plan_c, C.st);  // C = Q^T Y      (dense_kernels.cpp:399)
+      gemm_launch(plan_y, C.st);  // Y -= Q C       (dense_kernels.cpp:400)
+      panel_mgs(d_tasks, T, sweep, sweep == 1, bs, maxrows, C.st);
+    }
+  };
+  const char* ng = std::getenv("TLRG_NO_GRAPH");
+  if (ng && ng[0] == '1') {
+    // host-driven replay of the same static round (profiling / debugging)
+    int* h = C.pinned_ints(2);
+    for (int it = 0;; ++it) {
+      enqueue_round();
+      ara_loop_cond_host(active, C.st);
+      TLRG_CUDA(cudaMemcpyAsync(h, active, sizeof(int) * 2, cudaMemcpyDeviceToHost, C.st));
+      TLRG_CUDA(cudaStreamSynchronize(C.st));
+      if (h[0] <= 0 || it + 1 >= max_rounds) break;
+    }
+  } else {
+    cudaGraph_t graph = nullptr, body = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    TLRG_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle handle;
+    TLRG_CUDA(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    TLRG_CUDA(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+    body = cp.conditional.phGraph_out[0];
+    TLRG_CUDA(cudaStreamBeginCaptureToGraph(C.st, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeRelaxed));
+    enqueue_round();
+    ara_loop_cond(handle, active, max_rounds, C.st);
+    TLRG_CUDA(cudaStreamEndCapture(C.st, &body));
+    TLRG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    TLRG_CUDA(cudaGraphLaunch(exec, C.st));
+    graph_cleanup.push_back({exec, graph});
   }
-  ara_loop_cond(handle, active, max_rounds, C.st);
-  TLRG_CUDA(cudaStreamEndCapture(C.st, &body));
-  TLRG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-  TLRG_CUDA(cudaGraphLaunch(exec, C.st));
   tm.stop(C.st);
   std::vector<int> hq(T), h_rounds(T), h_conv(T), hact(2);
   std::vector<long long> hav(T), hcur(T);
@@ -236,8 +303,10 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   TLRG_CUDA(cudaMemcpyAsync(hcur.data(), G.cursor, sizeof(long long) * T, cudaMemcpyDeviceToHost,
                             C.st));
   C.sync();
-  cudaGraphExecDestroy(exec);
-  cudaGraphDestroy(graph);
+  for (auto& gc : graph_cleanup) {
+    cudaGraphExecDestroy(gc.first);
+    cudaGraphDestroy(gc.second);
+  }
   if (hact[0] > 0) throw CudaError("ara_batch: round limit reached with tiles still resident");
   C.launches += (long long)hact[1] * (4 + (long long)sample_plans.size() + 6);
   cst.t_sampling += tm.sec();  // the fused round loop (draws, sampling, orthog, absorb)
@@ -290,6 +359,13 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     std::vector<PanelTask> tasks;
     std::vector<SvdTask> svd;
     std::vector<int> sl;
+    std::vector<long long> roff2(T, 0);
+    long long rtot2 = 0;
+    for (int s = 0; s < T; ++s) {
+      roff2[s] = rtot2;
+      rtot2 += q[s];
+    }
+    double* rrep = C.buf<double>("rrep", (size_t)cols * rtot2 + 1);
     {
       std::vector<int> need_s;
       std::vector<long long> need;
@@ -313,6 +389,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       P.deficient = df + (size_t)s * qmax;
       P.gbuf = G.buf + (long long)s * G.cap;
       P.gcursor = G.cursor + s;
+      P.rep = rrep + (size_t)cols * roff2[s];
+      P.repC = nullptr;
       P.rows = cols;
       P.width = q[s];
       P.q = 0;

@@ -246,6 +246,7 @@ int tlrg_create(int device, tlrg_ctx* out, tlrg_status* st) {
     auto* c = new tlrg_ctx_s;
     c->c.device = device;
     TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.st, cudaStreamNonBlocking));
+    TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.st2, cudaStreamNonBlocking));
     c->c.desc.reserve(16 << 20);
     // one-time kernel attribute setup (never inside a graph capture)
     panel_mgs(nullptr, 0, 0, 0, 1, 1, c->c.st);
@@ -761,6 +762,8 @@ int tlrg_orthog(tlrg_ctx ctx, const double* Q, int32_t rows, int32_t q, double* 
     P.Y = dY; P.Q = q ? dQ : nullptr; P.R = dR; P.Rp = dRp; P.tiny = vec;
     P.col_norms = vec + k; P.new_mass = vec + 2 * k; P.deficient = df;
     P.gbuf = G.buf; P.gcursor = G.cursor;
+    P.rep = C.buf<double>("o_rep", (size_t)rows * k);
+    P.repC = C.buf<double>("o_repC", (size_t)(q + 1) * k);
     P.rows = rows; P.width = k; P.q = q;
     PanelTask* d = C.push(t);
     panel_tau(d, 1, C.st);

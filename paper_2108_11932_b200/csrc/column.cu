@@ -155,19 +155,10 @@ void column_H(Ctx& C, const Matrix& M, const ColumnSetup& cs, const std::vector<
   ++C.launches;
 }
 
-std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
-                                   const AraCfg& cfg, Store& store, ColumnStats& cst) {
-  const int nb = M.nb, b = M.b, rk = M.rows(k), bs = cfg.bs, K = cs.K;
-  std::vector<TileResult> res;
-  for (int i = k + 1; i < nb; ++i) {
-    TileResult r;
-    r.i = i;
-    res.push_back(r);
-  }
-  if (res.empty()) return res;
-  // rank-sorted order (ara.cpp:308-317)
+std::vector<int> column_queue(const Matrix& M, int k) {
   std::vector<int> order;
-  for (int i = k + 1; i < nb; ++i) order.push_back(i);
+  for (int i = k + 1; i < M.nb; ++i) order.push_back(i);
+  // large stored ranks first, ties by i (ara.cpp:308-317)
   std::stable_sort(order.begin(), order.end(), [&](int a, int c) {
     int ra = M.rank[M.t(a, k)], rc = M.rank[M.t(c, k)];
     if (ra != rc) return ra > rc;
@@ -181,6 +172,34 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
       if (M.rank[M.t(i, j)] > 0 && M.rank[M.t(k, j)] > 0) zero = false;
     if (!zero) queue.push_back(i);
   }
+  return queue;
+}
+
+void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPrep& P) {
+  std::vector<int> queue = column_queue(M, k);
+  std::vector<uint64_t> seeds;
+  int maxrows = 0;
+  for (int i : queue) {
+    seeds.push_back(ara_column_seed(cfg.seed, i, k));
+    maxrows = std::max(maxrows, M.rows(i));
+  }
+  P.T = 0;
+  if (queue.empty()) return;
+  streams_prepare(C, seeds, M.rows(k), cfg.bs, maxrows, 4, P);
+}
+
+std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
+                                   const AraCfg& cfg, Store& store, ColumnStats& cst,
+                                   StreamPrep* pre) {
+  const int nb = M.nb, b = M.b, rk = M.rows(k), bs = cfg.bs, K = cs.K;
+  std::vector<TileResult> res;
+  for (int i = k + 1; i < nb; ++i) {
+    TileResult r;
+    r.i = i;
+    res.push_back(r);
+  }
+  if (res.empty()) return res;
+  const std::vector<int> queue = column_queue(M, k);
   const int T = (int)queue.size();
   if (T == 0) return res;
 
@@ -313,7 +332,7 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
   for (int i = k + 1; i < nb; ++i)
     if (slot_of[i] >= 0) out_order.push_back(slot_of[i]);
   AraOut out;
-  ara_batch(C, S, op, cfg, store, out_order, cst, out);
+  ara_batch(C, S, op, cfg, store, out_order, cst, out, pre);
   for (int i = k + 1; i < nb; ++i) {
     TileResult& r = res[i - k - 1];
     int s = slot_of[i];

@@ -58,6 +58,7 @@ struct Store {
 struct Ctx {
   int device = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;  // side stream (gaussian stream pre-generation)
   DescArena desc;
   std::map<std::string, DevBuf> bufs;
   // pinned host staging for small D2H reads
@@ -225,15 +226,35 @@ struct AraOut {
   std::vector<int> rank, rounds, conv;
   std::vector<double*> U, V;
 };
+// Per-slot gaussian streams seeded and pre-generated on the side stream, so the
+// generation overlaps whatever the main stream does until the ARA starts.
+struct StreamPrep {
+  GaussStreams G;
+  cudaEvent_t ev = nullptr;
+  int T = 0;
+  long long pre = 0;  // values generated per slot
+  std::vector<uint64_t> seeds;
+  ~StreamPrep() {
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int bs, int maxrows,
+                     int rounds_ahead, StreamPrep& P);
 void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,
-               const std::vector<int>& out_order, ColumnStats& cst, AraOut& out);
+               const std::vector<int>& out_order, ColumnStats& cst, AraOut& out,
+               StreamPrep* pre = nullptr);
 
 // Dynamic-batched ARA over column k (chol_ara_update, ara.cpp:302-419): all
 // non-trivial tiles resident, converged tiles leave, exit projection and SVD
 // recompression batched at the end.  Results (ascending i) land in a panel
 // allocated from `store` (U: sum rows(i)*r, V: rk x sum r contiguous).
 std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
-                                   const AraCfg& cfg, Store& store, ColumnStats& cst);
+                                   const AraCfg& cfg, Store& store, ColumnStats& cst,
+                                   StreamPrep* pre = nullptr);
+// slot order of column k's ARA (rank-sorted, structural zeros removed) and the
+// early stream pre-generation for it (call at the start of the column)
+std::vector<int> column_queue(const Matrix& M, int k);
+void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPrep& P);
 
 struct FactorOpts {
   bool schur = true;

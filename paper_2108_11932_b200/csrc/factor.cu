@@ -191,6 +191,7 @@ void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint
     // replacement directions for rank-deficient sketch columns (not part of the
     // reference's streams): a counter-based gaussian pool consumed by cursor
     double* pool = C.buf<double>("sc_pool", (size_t)4 * n * p);
+    double* screp = C.buf<double>("sc_rep", (size_t)n * p);
     long long* pcur = C.buf<long long>("sc_pcur", 1);
     TLRG_CUDA(cudaMemsetAsync(pcur, 0, sizeof(long long), C.st));
     fill_gaussian_philox(pool, 4LL * n * p, mix64(seed ^ 0x5c1ULL) + attempt, C.st);
@@ -208,6 +209,7 @@ void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint
       P = PanelTask{};
       P.Y = X; P.Q = nullptr; P.R = R; P.Rp = Rp; P.tiny = vec; P.col_norms = vec + p;
       P.new_mass = vec + 2 * p; P.deficient = df; P.gbuf = pool; P.gcursor = pcur;
+      P.rep = screp; P.repC = nullptr;
       P.rows = n; P.width = p; P.q = 0;
       PanelTask* d = C.push(t);
       panel_tau(d, 1, C.st);
@@ -318,10 +320,14 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   int* info = C.buf<int>("finfo", 2);
   int rank_hint = 0;
   Ev e0, e1, e2, e3, e4, e5;
+  StreamPrep prep;
 
   for (int k = 0; k < nb; ++k) {
     const int rk = M.rows(k);
     double* diagk = M.diag + (size_t)k * b * b;
+    // ---- gaussian streams of this column's ARA, generated on the side stream
+    //      while the diagonal path runs
+    column_prepare(C, M, k, cfg, prep);
     // ---- dense phase: Gram blocks, H_k, D_k = sum_j L_kj [D_j] L_kj^T ----------
     cudaEventRecord(e0.e, C.st);
     ColumnSetup cs;
@@ -390,7 +396,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     S.t_compensation += comp_time;
     // ---- ARA over the column -------------------------------------------------
     ColumnStats cst;
-    std::vector<TileResult> res = column_ara(C, M, k, cs, cfg, *store, cst);
+    std::vector<TileResult> res = column_ara(C, M, k, cs, cfg, *store, cst, &prep);
     S.t_sampling += cst.t_sampling;
     S.t_orthog += cst.t_orthog;
     S.t_projection += cst.t_projection;

@@ -76,7 +76,13 @@ static GemmPlan plan_grouped(std::vector<GemmProblem>& probs, DescArena& desc, c
   plan.bn = BN;
   if (tiles == 0) return plan;
   if (tiles > 0x7fffffffLL) throw std::runtime_error("grouped_gemm: too many tiles");
+  std::vector<int> owner((size_t)tiles);
+  for (size_t p = 0; p < live.size(); ++p) {
+    long long t1 = p + 1 < live.size() ? live[p + 1].tile_start : tiles;
+    for (long long t = live[p].tile_start; t < t1; ++t) owner[t] = (int)p;
+  }
   plan.d = (const GemmProblem*)desc.push(live.data(), live.size() * sizeof(GemmProblem), st);
+  plan.owner = (const int*)desc.push(owner.data(), owner.size() * sizeof(int), st);
   plan.n = (int)live.size();
   plan.tiles = (int)tiles;
   return plan;
@@ -92,9 +98,9 @@ GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_
 void gemm_launch(const GemmPlan& p, cudaStream_t st) {
   if (p.tiles == 0) return;
   if (p.bn == 16)
-    grouped_gemm_kernel<64, 16><<<(unsigned)p.tiles, 128, 0, st>>>(p.d, p.n);
+    grouped_gemm_kernel<64, 16><<<(unsigned)p.tiles, 128, 0, st>>>(p.d, p.owner);
   else
-    grouped_gemm_kernel<64, 32><<<(unsigned)p.tiles, 128, 0, st>>>(p.d, p.n);
+    grouped_gemm_kernel<64, 32><<<(unsigned)p.tiles, 128, 0, st>>>(p.d, p.owner);
   TLRG_CUDA(cudaGetLastError());
 }
 

@@ -36,6 +36,8 @@ struct GemmProblem {
   const int* Kp;
 };
 
+static_assert(sizeof(GemmProblem) % 8 == 0 && sizeof(GemmProblem) / 8 <= 128, "descriptor");
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   int sz = valid ? 8 : 0;
@@ -58,30 +60,40 @@ struct GemmCfg {
 
 template <int BM, int BN>
 __global__ void __launch_bounds__(128) grouped_gemm_kernel(const GemmProblem* __restrict__ probs,
-                                                           int nprob) {
+                                                           const int* __restrict__ owner) {
   using Cfg = GemmCfg<BM, BN>;
   constexpr int BK = Cfg::BK, SA = Cfg::SA, SB = Cfg::SB;
   __shared__ __align__(16) double As[2][BK * SA];
   __shared__ __align__(16) double Bs[2][BK * SB];
-  __shared__ int s_prob;
+  __shared__ __align__(16) GemmProblem sP;
+  __shared__ int s_go;
 
-  // locate the problem owning this CTA (binary search on tile_start)
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = nprob - 1, t = blockIdx.x;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (probs[mid].tile_start <= t) lo = mid; else hi = mid - 1;
+  // the problem owning this CTA comes from a per-CTA owner table; the 8-byte
+  // words of its descriptor are fetched in parallel and the device-side
+  // controls are resolved once
+  {
+    const int pidx = owner[blockIdx.x];
+    const unsigned long long* src =
+        reinterpret_cast<const unsigned long long*>(probs + pidx);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sP);
+    constexpr int W = sizeof(GemmProblem) / 8;
+    if (threadIdx.x < W) dst[threadIdx.x] = src[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int go = 1;
+      if (sP.skip && *sP.skip) go = 0;
+      if (go && sP.Mp) sP.M = min(sP.M, *sP.Mp);
+      if (go && sP.Kp) sP.K = min(sP.K, *sP.Kp);
+      const int local = blockIdx.x - sP.tile_start;
+      if (go && (local / sP.tiles_n) * BM >= sP.M) go = 0;
+      s_go = go;
     }
-    s_prob = lo;
+    __syncthreads();
+    if (!s_go) return;
   }
-  __syncthreads();
-  GemmProblem P = probs[s_prob];
+  const GemmProblem P = sP;
   const int local = blockIdx.x - P.tile_start;
   const int m0 = (local / P.tiles_n) * BM, n0 = (local % P.tiles_n) * BN;
-  if (P.skip && *P.skip) return;
-  if (P.Mp) P.M = min(P.M, *P.Mp);
-  if (P.Kp) P.K = min(P.K, *P.Kp);
-  if (m0 >= P.M) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 1) * Cfg::WM, wn = (warp & 1) * Cfg::WN;
   const int g = lane >> 2, t4 = lane & 3;

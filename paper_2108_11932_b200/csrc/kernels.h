@@ -19,6 +19,7 @@ void grouped_gemm(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t
 // Two-step form: stage the table once (before a graph capture), launch many times.
 struct GemmPlan {
   const GemmProblem* d = nullptr;
+  const int* owner = nullptr;  // per-CTA problem index
   int n = 0, tiles = 0, bn = 32;
 };
 GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st);
@@ -79,6 +80,8 @@ struct PanelTask {
   double* new_mass;   // width
   const double* gbuf; // tile's gaussian stream (deficient-column replacements)
   long long* gcursor; // its cursor (device)
+  double* rep;        // rows x width scratch: projected replacement directions
+  double* repC;       // q x width scratch (Q^T rep)
   double tau;         // 100 * DBL_EPSILON * ||Y_raw||_F (or DBL_MIN)
   int rows, width, q;
   // device-driven ARA round (all optional): skip when *done, basis width from

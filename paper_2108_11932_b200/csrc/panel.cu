@@ -436,6 +436,8 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
     }
   __syncthreads();
   const double tau = T.tau;
+  int rep_n = 0, rep_used = 0;  // batch of projected replacement vectors
+  long long rep_base = 0;
 
   for (int j = 0; j < w; ++j) {
     double* yj = Y + (long long)j * rows;
@@ -453,30 +455,43 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
         T.deficient[j] = 1;
         T.tiny[j] = isfinite(nj) ? nj : 0.0;
       }
-      {
-        // the next `rows` values of the tile's stream (dense_kernels.cpp:351)
+      if (rep_used == rep_n) {
+        // Project the next (w - j) vectors of the tile's stream against Q in
+        // one batch: replacement vector u is stream[c0 + u*rows, ...) with
+        // y <- y - Q (Q^T y) (dense_kernels.cpp:351-358); the cursor only
+        // advances over the vectors actually consumed.
+        __syncthreads();
         const long long c0 = *T.gcursor;
+        rep_base = c0;
+        rep_used = 0;
+        rep_n = w - j;
         __syncthreads();
-        for (int r = tid; r < rows; r += PT) yj[r] = T.gbuf[c0 + r];
-        if (tid == 0) *T.gcursor = c0 + rows;
-      }
-      __syncthreads();
-      if (q > 0) {
-        for (int t = warp; t < q; t += PW) {
-          const double* qt = T.Q + (long long)t * rows;
-          double s = 0.0;
-          for (int r = lane; r < rows; r += 32) s += qt[r] * yj[r];
-          s = warp_sum(s);
-          if (lane == 0) S.cbuf[t] = s;
+        for (long long e = tid; e < (long long)rows * rep_n; e += PT) T.rep[e] = T.gbuf[c0 + e];
+        __syncthreads();
+        if (q > 0) {
+          for (int pi = warp; pi < q * rep_n; pi += PW) {
+            const int t = pi % q, c = pi / q;
+            const double* qt = T.Q + (long long)t * rows;
+            const double* rc = T.rep + (long long)c * rows;
+            double s = 0.0;
+            for (int r = lane; r < rows; r += 32) s += qt[r] * rc[r];
+            s = warp_sum(s);
+            if (lane == 0) T.repC[t + (long long)c * q] = s;
+          }
+          __syncthreads();
+          for (int r = tid; r < rows; r += PT)
+            for (int c = 0; c < rep_n; ++c) {
+              double s = 0.0;
+              for (int t = 0; t < q; ++t)
+                s += T.Q[(long long)t * rows + r] * T.repC[t + (long long)c * q];
+              T.rep[r + (long long)c * rows] -= s;
+            }
+          __syncthreads();
         }
-        __syncthreads();
-        for (int r = tid; r < rows; r += PT) {
-          double s = 0.0;
-          for (int t = 0; t < q; ++t) s += T.Q[(long long)t * rows + r] * S.cbuf[t];
-          yj[r] -= s;
-        }
-        __syncthreads();
       }
+      for (int r = tid; r < rows; r += PT) yj[r] = T.rep[r + (long long)rep_used * rows];
+      ++rep_used;
+      if (tid == 0) *T.gcursor = rep_base + (long long)rep_used * rows;
       if (j > 0)
         for (int pass = 0; pass < 2; ++pass) cgs_pass(Y, rows, j, S);
       nj = col_norm(yj, rows, S);

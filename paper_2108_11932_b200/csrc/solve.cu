@@ -468,6 +468,8 @@ Ctx::~Ctx() {
   if (h_dbl) cudaFreeHost(h_dbl);
   bufs.clear();
   if (st) cudaStreamDestroy(st);
+  if (st2) cudaStreamDestroy(st2);
+  for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
 }
 void Matrix::free_all() {
   if (diag) cudaFree(diag);
