@@ -63,12 +63,13 @@ void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int b
   P.seeds = seeds;
   GaussStreams& G = P.G;
   G.st = C.buf<RngState>("p_rng", (size_t)T);
-  G.cap = 6LL * cols * bs + 4LL * bs * maxrows;
+  G.cap = (12LL * cols * bs + 4LL * bs * maxrows + 1) & ~1LL;
   G.buf = C.buf<double>("p_gbuf", (size_t)T * G.cap);
   long long* gl = C.buf<long long>("p_gcur", (size_t)2 * T);
   G.avail = gl;
   G.cursor = gl + T;
   P.pre = std::min<long long>(G.cap, (long long)rounds_ahead * cols * bs + 2LL * bs * maxrows);
+  (void)0;
   P.pre &= ~1LL;
   uint64_t* d_seeds = C.buf<uint64_t>("p_seeds", (size_t)T);
   int* d_slots = C.buf<int>("p_slots", (size_t)T);
@@ -124,13 +125,13 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   GaussStreams G;
   std::vector<long long> h_av(T, 0), h_cur(T, 0);
   if (pre && pre->T == T && pre->seeds == S.seeds &&
-      pre->G.cap >= 6LL * cols * bs + 4LL * bs * maxrows) {
+      pre->G.cap >= 2LL * cols * bs + 4LL * bs * maxrows) {
     G = pre->G;
     TLRG_CUDA(cudaStreamWaitEvent(C.st, pre->ev, 0));
     for (int s = 0; s < T; ++s) h_av[s] = pre->pre;
   } else {
     G.st = C.buf<RngState>("rng", (size_t)T);
-    G.cap = 6LL * cols * bs + 4LL * bs * maxrows;
+    G.cap = (6LL * cols * bs + 4LL * bs * maxrows + 1) & ~1LL;
     G.buf = C.buf<double>("gbuf", (size_t)T * G.cap);
     long long* gl = C.buf<long long>("gcur", (size_t)2 * T);
     G.avail = gl;
@@ -142,26 +143,15 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   const long long gchunk = 2LL * cols * bs;
   // make sure every listed slot has `need` values ready beyond its cursor
   auto ensure = [&](const std::vector<int>& slots, const std::vector<long long>& need) {
-    std::vector<int> gen, cmp;
+    std::vector<int> gen;
     std::vector<long long> want;
     for (size_t t = 0; t < slots.size(); ++t) {
       int s = slots[t];
       if (h_av[s] - h_cur[s] >= need[t]) continue;
-      if (G.cap - h_cur[s] < need[t] + gchunk) {
-        cmp.push_back(s);
-        h_av[s] -= h_cur[s];
-        h_cur[s] = 0;
-      }
-      long long w = std::min(G.cap, h_cur[s] + need[t] + gchunk);
-      w = (w + 1) & ~1LL;
-      if (w > G.cap) w = G.cap & ~1LL;
+      long long w = std::min(h_cur[s] + G.cap, h_cur[s] + need[t] + gchunk) & ~1LL;
       gen.push_back(s);
       want.push_back(w);
       h_av[s] = w;
-    }
-    if (!cmp.empty()) {
-      gauss_compact(G, C.push(cmp), (int)cmp.size(), C.st);
-      ++C.launches;
     }
     if (!gen.empty()) {
       gauss_generate(G, C.push(gen), C.push(want), (int)gen.size(), C.st);
@@ -218,6 +208,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     P.new_mass = nm + (size_t)s * bs;
     P.gbuf = G.buf + (long long)s * G.cap;
     P.gcursor = G.cursor + s;
+    P.gcap = G.cap;
     P.rep = rep + (size_t)s * maxrows * bs;
     P.repC = repC + (size_t)s * capmax * bs;
     P.rows = S.rows[s];
@@ -389,6 +380,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       P.deficient = df + (size_t)s * qmax;
       P.gbuf = G.buf + (long long)s * G.cap;
       P.gcursor = G.cursor + s;
+      P.gcap = G.cap;
       P.rep = rrep + (size_t)cols * roff2[s];
       P.repC = nullptr;
       P.rows = cols;

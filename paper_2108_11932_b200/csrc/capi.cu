@@ -742,7 +742,7 @@ int tlrg_orthog(tlrg_ctx ctx, const double* Q, int32_t rows, int32_t q, double* 
     double* vec = C.buf<double>("o_vec", (size_t)4 * k);
     uint8_t* df = C.buf<uint8_t>("o_df", (size_t)k);
     GaussStreams G;
-    G.cap = 2LL * k * rows + 4;
+    G.cap = (2LL * k * rows + 4) & ~1LL;
     G.st = C.buf<RngState>("o_rng", 1);
     G.buf = C.buf<double>("o_gbuf", (size_t)G.cap);
     long long* gl = C.buf<long long>("o_gcur", 2);
@@ -761,7 +761,7 @@ int tlrg_orthog(tlrg_ctx ctx, const double* Q, int32_t rows, int32_t q, double* 
     P = PanelTask{};
     P.Y = dY; P.Q = q ? dQ : nullptr; P.R = dR; P.Rp = dRp; P.tiny = vec;
     P.col_norms = vec + k; P.new_mass = vec + 2 * k; P.deficient = df;
-    P.gbuf = G.buf; P.gcursor = G.cursor;
+    P.gbuf = G.buf; P.gcursor = G.cursor; P.gcap = G.cap;
     P.rep = C.buf<double>("o_rep", (size_t)rows * k);
     P.repC = C.buf<double>("o_repC", (size_t)(q + 1) * k);
     P.rows = rows; P.width = k; P.q = q;

@@ -185,7 +185,7 @@ void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPre
   }
   P.T = 0;
   if (queue.empty()) return;
-  streams_prepare(C, seeds, M.rows(k), cfg.bs, maxrows, 4, P);
+  streams_prepare(C, seeds, M.rows(k), cfg.bs, maxrows, 8, P);
 }
 
 std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,

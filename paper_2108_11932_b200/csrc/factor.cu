@@ -209,7 +209,7 @@ void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint
       P = PanelTask{};
       P.Y = X; P.Q = nullptr; P.R = R; P.Rp = Rp; P.tiny = vec; P.col_norms = vec + p;
       P.new_mass = vec + 2 * p; P.deficient = df; P.gbuf = pool; P.gcursor = pcur;
-      P.rep = screp; P.repC = nullptr;
+      P.rep = screp; P.repC = nullptr; P.gcap = 4LL * n * p;
       P.rows = n; P.width = p; P.q = 0;
       PanelTask* d = C.push(t);
       panel_tau(d, 1, C.st);

@@ -43,9 +43,10 @@ void rng_seed(RngState* states, const uint64_t* d_seeds, int n, cudaStream_t st)
 void rng_draw(RngState* states, const int* d_state_idx, int ntiles, double* out,
               long long count, long long out_stride, cudaStream_t st);
 
-// Per-tile Gaussian streams (pre-generated, consumed by cursor).  The stream of
-// slot s is the exact tlr::Rng(seed_s).gaussian() sequence; generation always
-// appends whole polar pairs, so no pair cache is needed.
+// Per-tile Gaussian streams (pre-generated ring buffers, consumed by cursor).
+// The stream of slot s is the exact tlr::Rng(seed_s).gaussian() sequence;
+// generation always appends whole polar pairs, so no pair cache is needed.
+// Capacities must be even.
 struct GaussStreams {
   RngState* st = nullptr;     // generator state, positioned after avail[s] values
   double* buf = nullptr;      // slot s at buf + s*cap
@@ -59,8 +60,6 @@ void gauss_generate(const GaussStreams& G, const int* d_slots, const long long* 
 // out + a*out_stride <- next `count` values of slot d_slots[a]; advances cursors
 void gauss_gather(const GaussStreams& G, const int* d_slots, int n, double* out, long long count,
                   long long out_stride, cudaStream_t st);
-// move [cursor, avail) to the front of each listed slot
-void gauss_compact(const GaussStreams& G, const int* d_slots, int n, cudaStream_t st);
 // one ARA round's draws for ALL slots (skipping done ones): top the stream up
 // (compacting when needed) so that this round's Omega and every possible
 // deficient-column replacement are available, then copy Omega_s to Om + s*cols*bs.
@@ -80,6 +79,7 @@ struct PanelTask {
   double* new_mass;   // width
   const double* gbuf; // tile's gaussian stream (deficient-column replacements)
   long long* gcursor; // its cursor (device)
+  long long gcap;     // ring capacity of the stream
   double* rep;        // rows x width scratch: projected replacement directions
   double* repC;       // q x width scratch (Q^T rep)
   double tau;         // 100 * DBL_EPSILON * ||Y_raw||_F (or DBL_MIN)

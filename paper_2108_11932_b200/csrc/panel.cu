@@ -131,6 +131,8 @@ void rng_draw(RngState* states, const int* d_idx, int ntiles, double* out, long 
 }
 
 // ------------------------------------------------------------ STREAMS ----
+// Ring buffers: absolute stream position p lives at buf[s*cap + p % cap];
+// avail / cursor are absolute counts with avail - cursor <= cap.
 struct GenSmem {
   uint64_t mt[MT_N];
   double pu[RCH], pv[RCH], ps[RCH];
@@ -193,8 +195,9 @@ __device__ void cta_generate(GaussStreams& G, int s, long long have, long long t
     for (int i = tid; i < chunk; i += blockDim.x) {
       double q = S.ps[i];
       double f = sqrt(-2.0 * log(q) / q);
-      buf[have + 2 * i] = S.pu[i] * f;
-      buf[have + 2 * i + 1] = S.pv[i] * f;
+      long long p0 = have + 2 * i;  // even, cap even: the pair never wraps apart
+      buf[p0 % G.cap] = S.pu[i] * f;
+      buf[(p0 + 1) % G.cap] = S.pv[i] * f;
     }
     have += 2LL * chunk;
     __syncthreads();
@@ -208,14 +211,18 @@ __device__ void cta_generate(GaussStreams& G, int s, long long have, long long t
   __syncthreads();
 }
 
+__device__ __forceinline__ long long ring_target(const GaussStreams& G, long long cur,
+                                                 long long want) {
+  long long t = want < cur + G.cap ? want : cur + G.cap;
+  return t & ~1LL;
+}
+
 __global__ void __launch_bounds__(RT) gauss_generate_kernel(GaussStreams G, const int* slots,
                                                             const long long* want) {
   __shared__ GenSmem S;
   const int s = slots[blockIdx.x];
-  long long have = G.avail[s];
-  long long target = want[blockIdx.x];
-  if (target > G.cap) target = G.cap;
-  target &= ~1LL;
+  const long long have = G.avail[s];
+  const long long target = ring_target(G, G.cursor[s], want[blockIdx.x]);
   if (have >= target) return;
   cta_generate(G, s, have, target, S);
 }
@@ -228,40 +235,14 @@ __global__ void __launch_bounds__(RT) gauss_round_kernel(GaussStreams G, const i
   if (done[s]) return;
   const long long need = (long long)cols * bs + 2LL * bs * rows[s];
   const long long chunk = 2LL * cols * bs;
-  long long cur = G.cursor[s], av = G.avail[s];
-  double* b = G.buf + (long long)s * G.cap;
-  if (av - cur < need) {
-    if (G.cap - cur < need + chunk && cur > 0) {
-      // compact [cur, av) to the front (forward copy, destination below source)
-      for (long long base = 0; base < av - cur; base += RT) {
-        long long e = base + threadIdx.x;
-        double v = e < av - cur ? b[cur + e] : 0.0;
-        __syncthreads();
-        if (e < av - cur) b[e] = v;
-        __syncthreads();
-      }
-      av -= cur;
-      cur = 0;
-      if (threadIdx.x == 0) G.cursor[s] = 0;
-    }
-    long long target = cur + need + chunk;
-    if (target > G.cap) target = G.cap;
-    target = (target + 1) & ~1LL;
-    if (target > G.cap) target -= 2;
-    cta_generate(G, s, av, target, S);
-  }
-  const double* src = b + cur;
+  const long long cur = G.cursor[s], av = G.avail[s];
+  if (av - cur < need) cta_generate(G, s, av, ring_target(G, cur, cur + need + chunk), S);
+  const double* b = G.buf + (long long)s * G.cap;
   double* dst = Om + (long long)s * cols * bs;
-  for (long long e = threadIdx.x; e < (long long)cols * bs; e += RT) dst[e] = src[e];
+  const long long n = (long long)cols * bs;
+  for (long long e = threadIdx.x; e < n; e += RT) dst[e] = b[(cur + e) % G.cap];
   __syncthreads();
-  if (threadIdx.x == 0) G.cursor[s] = cur + (long long)cols * bs;
-}
-
-void gauss_round(const GaussStreams& G, const int* done, const int* rows, int nslots, int cols,
-                 int bs, double* Om, cudaStream_t st) {
-  if (nslots <= 0) return;
-  gauss_round_kernel<<<nslots, RT, 0, st>>>(G, done, rows, cols, bs, Om);
-  TLRG_CUDA(cudaGetLastError());
+  if (threadIdx.x == 0) G.cursor[s] = cur + n;
 }
 
 __global__ void __launch_bounds__(256) gauss_gather_kernel(GaussStreams G, const int* slots,
@@ -269,29 +250,11 @@ __global__ void __launch_bounds__(256) gauss_gather_kernel(GaussStreams G, const
                                                            long long out_stride) {
   const int s = slots[blockIdx.x];
   const long long c0 = G.cursor[s];
-  const double* src = G.buf + (long long)s * G.cap + c0;
+  const double* b = G.buf + (long long)s * G.cap;
   double* dst = out + (long long)blockIdx.x * out_stride;
-  for (long long e = threadIdx.x; e < count; e += 256) dst[e] = src[e];
+  for (long long e = threadIdx.x; e < count; e += 256) dst[e] = b[(c0 + e) % G.cap];
   __syncthreads();
   if (threadIdx.x == 0) G.cursor[s] = c0 + count;
-}
-
-__global__ void __launch_bounds__(256) gauss_compact_kernel(GaussStreams G, const int* slots) {
-  const int s = slots[blockIdx.x];
-  const long long c0 = G.cursor[s], a = G.avail[s];
-  double* b = G.buf + (long long)s * G.cap;
-  // forward copy is safe: destination index < source index
-  for (long long base = 0; base < a - c0; base += 256) {
-    long long e = base + threadIdx.x;
-    double v = e < a - c0 ? b[c0 + e] : 0.0;
-    __syncthreads();
-    if (e < a - c0) b[e] = v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    G.cursor[s] = 0;
-    G.avail[s] = a - c0;
-  }
 }
 
 void gauss_generate(const GaussStreams& G, const int* d_slots, const long long* d_want, int n,
@@ -306,9 +269,10 @@ void gauss_gather(const GaussStreams& G, const int* d_slots, int n, double* out,
   gauss_gather_kernel<<<n, 256, 0, st>>>(G, d_slots, out, count, out_stride);
   TLRG_CUDA(cudaGetLastError());
 }
-void gauss_compact(const GaussStreams& G, const int* d_slots, int n, cudaStream_t st) {
-  if (n <= 0) return;
-  gauss_compact_kernel<<<n, 256, 0, st>>>(G, d_slots);
+void gauss_round(const GaussStreams& G, const int* done, const int* rows, int nslots, int cols,
+                 int bs, double* Om, cudaStream_t st) {
+  if (nslots <= 0) return;
+  gauss_round_kernel<<<nslots, RT, 0, st>>>(G, done, rows, cols, bs, Om);
   TLRG_CUDA(cudaGetLastError());
 }
 
@@ -390,11 +354,23 @@ __device__ __forceinline__ void cgs_pass(double* Y, int rows, int j, PanelSmem& 
     if (lane == 0) S.cbuf[p] = sa;
   }
   __syncthreads();
+  // y_j -= sum_p c_p y_p over this thread's rows (independent accumulators per row)
   double* yw = Y + (long long)j * rows;
-  for (int r = threadIdx.x; r < rows; r += PT) {
-    double s = 0.0;
-    for (int p = 0; p < j; ++p) s += S.cbuf[p] * Y[(long long)p * rows + r];
-    yw[r] -= s;
+  constexpr int RPT = 8;
+  for (int r0 = 0; r0 < rows; r0 += RPT * PT) {
+    double acc[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) acc[u] = 0.0;
+    for (int p = 0; p < j; ++p) {
+      const double c = S.cbuf[p];
+      const double* yp = Y + (long long)p * rows + r0 + threadIdx.x;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+        if (r0 + threadIdx.x + u * PT < rows) acc[u] += c * yp[u * PT];
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u)
+      if (r0 + threadIdx.x + u * PT < rows) yw[r0 + threadIdx.x + u * PT] -= acc[u];
   }
 }
 
@@ -425,9 +401,26 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
   const int rows = T.rows, w = T.width, q = T.qdev ? *T.qdev : T.q;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* Rp = rp_in_smem ? dyn : T.Rp;
-  double* Y = ys_in_smem ? dyn + (rp_in_smem ? (size_t)w * w : 0) : T.Y;
-  if (ys_in_smem)
-    for (long long e = tid; e < (long long)rows * w; e += PT) Y[e] = T.Y[e];
+  size_t yoff = rp_in_smem ? (size_t)w * w : 0;
+  yoff += (smem_u32(dyn + yoff) & 15) ? 1 : 0;  // 16-byte aligned panel
+  double* Y = ys_in_smem ? dyn + yoff : T.Y;
+  const unsigned ybytes = (unsigned)((size_t)rows * w * 8);
+  const bool bulk = ys_in_smem && (ybytes % 16 == 0) && (((size_t)T.Y & 15) == 0);
+  __shared__ __align__(8) uint64_t s_bar;
+  if (ys_in_smem) {
+    if (bulk) {
+      // one TMA bulk copy stages the whole panel (UBLKCP)
+      if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        mbar_arrive_expect_tx(&s_bar, ybytes);
+        bulk_g2s(Y, T.Y, ybytes, &s_bar);
+      }
+      __syncthreads();
+      mbar_wait(&s_bar, 0);
+    } else {
+      for (long long e = tid; e < (long long)rows * w; e += PT) Y[e] = T.Y[e];
+    }
+  }
   for (long long e = tid; e < (long long)w * w; e += PT) Rp[e] = 0.0;
   if (sweep == 0)
     for (int j = tid; j < w; j += PT) {
@@ -466,7 +459,8 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
         rep_used = 0;
         rep_n = w - j;
         __syncthreads();
-        for (long long e = tid; e < (long long)rows * rep_n; e += PT) T.rep[e] = T.gbuf[c0 + e];
+        for (long long e = tid; e < (long long)rows * rep_n; e += PT)
+          T.rep[e] = T.gbuf[(c0 + e) % T.gcap];
         __syncthreads();
         if (q > 0) {
           for (int pi = warp; pi < q * rep_n; pi += PW) {
@@ -507,9 +501,18 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
     const double inv = 1.0 / nj;
     for (int r = tid; r < rows; r += PT) yj[r] *= inv;
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
   __syncthreads();
-  if (ys_in_smem && !(finalize && T.qcols))
-    for (long long e = tid; e < (long long)rows * w; e += PT) T.Y[e] = Y[e];
+  if (ys_in_smem && !(finalize && T.qcols)) {
+    if (bulk) {
+      if (tid == 0) {
+        bulk_s2g(T.Y, Y, ybytes);
+        bulk_wait_all();
+      }
+    } else {
+      for (long long e = tid; e < (long long)rows * w; e += PT) T.Y[e] = Y[e];
+    }
+  }
 
   // R <- Rp * R  (R = I before the first sweep)
   double* R = T.R;
@@ -592,8 +595,8 @@ void panel_mgs(PanelTask* d_tasks, int ntask, int sweep, int finalize, int max_w
   size_t rp = (size_t)max_width * max_width * 8;
   size_t ys = (size_t)max_rows * max_width * 8;
   int rp_in = base + rp <= lim;
-  int ys_in = base + (rp_in ? rp : 0) + ys <= lim;
-  size_t bytes = base + (rp_in ? rp : 0) + (ys_in ? ys : 0);
+  int ys_in = base + (rp_in ? rp : 0) + ys + 16 <= lim;
+  size_t bytes = base + (rp_in ? rp : 0) + (ys_in ? ys + 16 : 0);
   panel_mgs_kernel<<<ntask, PT, bytes, st>>>(d_tasks, sweep, finalize, ys_in, rp_in, part_len,
                                              cbuf_len);
   TLRG_CUDA(cudaGetLastError());
