@@ -251,7 +251,6 @@ int tlrg_create(int device, tlrg_ctx* out, tlrg_status* st) {
     // one-time kernel attribute setup (never inside a graph capture)
     panel_mgs(nullptr, 0, 0, 0, 1, 1, c->c.st);
     jacobi_svd(nullptr, 0, 1, c->c.st);
-    trsm_panel(nullptr, 0, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr, c->c.st);
     *out = c;
   });
 }

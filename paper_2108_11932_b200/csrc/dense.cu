@@ -6,6 +6,7 @@
 //   * panel TRSM X = L^{-1} B (dense_kernels.cpp:311-322) shared by all tiles of
 //     a column, with the LDL row permutation and D^{-1} fused (factor.cpp:257-262).
 //   * small helpers: symmetrize, diagonal combine, pivot traces, D apply.
+#include <algorithm>
 #include <cfloat>
 
 #include <cooperative_groups.h>
@@ -17,130 +18,162 @@ namespace cg = cooperative_groups;
 namespace tlrg {
 
 // ---------------------------------------------------------------- POTRF ---
-// Left-looking blocked Cholesky in ONE cooperative kernel: CTA r owns the
-// 32-row block r.  Per 32-column panel p:
-//   update : A[r, p] -= L[r, 0:p] L[p, 0:p]^T      (CTAs r >= p, in parallel)
-//   grid.sync
-//   factor : every CTA factors A_pp redundantly in shared memory (one warp),
-//            CTA p stores L_pp, CTAs r > p solve X L_pp^T = A[r, p]
-//   grid.sync
+// Right-looking blocked Cholesky in ONE cooperative kernel over a persistent
+// grid.  Per 32-column panel p:
+//   phase 1: for each row block r >= p (CTAs in parallel) factor A_pp in shared
+//            memory (redundantly, one warp) and store L_pp (r = p) or solve
+//            L_rp = A_rp L_pp^{-T} (r > p);                       grid.sync
+//   phase 2: rank-32 update of every trailing lower tile
+//            A_rc -= L_rp L_cp^T, p < c <= r, spread over all CTAs; grid.sync
 constexpr int PB = 32;
 constexpr int PO_T = 128;
+
+__device__ __forceinline__ bool chol32_smem(double (*Lp)[PB + 1], int pw, int* fail_at) {
+  // unblocked right-looking Cholesky of the pw x pw block held by warp 0
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < pw; ++j) {
+    double d = Lp[j][j];
+    if (!(d > 0.0)) {
+      *fail_at = j;
+      return false;
+    }
+    double s = sqrt(d);
+    __syncwarp();
+    if (lane == 0) Lp[j][j] = s;
+    __syncwarp();
+    if (lane > j && lane < pw) Lp[lane][j] /= s;
+    __syncwarp();
+    if (lane > j && lane < pw)
+      for (int c = j + 1; c <= lane; ++c) Lp[lane][c] -= Lp[lane][j] * Lp[c][j];
+    __syncwarp();
+  }
+  return true;
+}
 
 __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int* info) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double Lp[PB][PB + 1];
   __shared__ double Ar[PB][PB + 1];
-  __shared__ double La[PB][PB + 1];
   __shared__ double Lb[PB][PB + 1];
-  __shared__ int fail;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int r = blockIdx.x;            // row block
-  const int r0 = r * PB;
-  const int rw = min(PB, n - r0);
-  const int np = (n + PB - 1) / PB;
-  if (tid == 0) fail = -1;
-  for (int p = 0; p < np; ++p) {
-    const int p0 = p * PB, pw = min(PB, n - p0);
-    if (r >= p) {
-      // ---- update A[r, p] -= L[r, 0:p0] L[p, 0:p0]^T (thread: 8 outputs) ----
-      double acc[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) acc[t] = 0.0;
-      const int ci = tid & 31, rj = tid >> 5;  // column ci of the block, rows rj + 4t
-      for (int k0 = 0; k0 < p0; k0 += PB) {
-        for (int e = tid; e < PB * PB; e += PO_T) {
-          int i = e % PB, k = e / PB;
-          La[i][k] = i < rw ? A[(r0 + i) + (long long)(k0 + k) * n] : 0.0;
-          Lb[i][k] = i < pw ? A[(p0 + i) + (long long)(k0 + k) * n] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int k = 0; k < PB; ++k) {
-          double bv = Lb[ci][k];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) acc[t] += La[rj + 4 * t][k] * bv;
-        }
-        __syncthreads();
-      }
-      if (p0 > 0)
-        for (int t = 0; t < 8; ++t) {
-          int i = rj + 4 * t;
-          if (i < rw && ci < pw) A[(r0 + i) + (long long)(p0 + ci) * n] -= acc[t];
-        }
-    }
-    grid.sync();
-    if (r >= p) {
+  __shared__ int s_fail;
+  const int tid = threadIdx.x;
+  const int nt = (n + PB - 1) / PB;
+  auto bw = [&](int t) { return min(PB, n - t * PB); };
+  for (int p = 0; p < nt; ++p) {
+    const int p0 = p * PB, pw = bw(p);
+    // ---- phase 1 -------------------------------------------------------------
+    for (int r = p + blockIdx.x; r < nt; r += gridDim.x) {
+      const int r0 = r * PB, rw = bw(r);
+      __syncthreads();
       for (int e = tid; e < PB * PB; e += PO_T) {
         int i = e % PB, j = e / PB;
         Lp[i][j] = (i < pw && j < pw) ? A[(p0 + i) + (long long)(p0 + j) * n] : 0.0;
       }
+      if (tid == 0) s_fail = -1;
       __syncthreads();
       if (tid < 32) {
-        for (int j = 0; j < pw; ++j) {
-          double d = Lp[j][j];
-          if (!(d > 0.0)) {
-            if (lane == 0) fail = p0 + j;
-            break;
-          }
-          double s = sqrt(d);
-          __syncwarp();
-          if (lane == 0) Lp[j][j] = s;
-          __syncwarp();
-          if (lane > j && lane < pw) Lp[lane][j] /= s;
-          __syncwarp();
-          if (lane > j && lane < pw)
-            for (int c = j + 1; c <= lane; ++c) Lp[lane][c] -= Lp[lane][j] * Lp[c][j];
-          __syncwarp();
-        }
+        int fa = -1;
+        bool ok = chol32_smem(Lp, pw, &fa);
+        if (!ok && tid == 0) s_fail = p0 + fa;
       }
       __syncthreads();
-      if (fail < 0) {
-        if (r == p) {
-          for (int e = tid; e < pw * pw; e += PO_T) {
-            int i = e % pw, j = e / pw;
-            A[(p0 + i) + (long long)(p0 + j) * n] = i >= j ? Lp[i][j] : 0.0;
+      if (s_fail >= 0) {
+        if (tid == 0) atomicCAS(info, -1, s_fail);
+        continue;
+      }
+      if (r == p) {
+        for (int e = tid; e < pw * pw; e += PO_T) {
+          int i = e % pw, j = e / pw;
+          A[(p0 + i) + (long long)(p0 + j) * n] = i >= j ? Lp[i][j] : 0.0;
+        }
+      } else {
+        for (int e = tid; e < rw * pw; e += PO_T) {
+          int i = e % rw, j = e / rw;
+          Ar[i][j] = A[(r0 + i) + (long long)(p0 + j) * n];
+        }
+        __syncthreads();
+        if (tid < rw)
+          for (int j = 0; j < pw; ++j) {
+            double s = Ar[tid][j];
+            for (int t = 0; t < j; ++t) s -= Ar[tid][t] * Lp[j][t];
+            Ar[tid][j] = s / Lp[j][j];
           }
-        } else {
-          for (int e = tid; e < rw * pw; e += PO_T) {
-            int i = e % rw, j = e / rw;
-            Ar[i][j] = A[(r0 + i) + (long long)(p0 + j) * n];
-          }
-          __syncthreads();
-          if (tid < rw)
-            for (int j = 0; j < pw; ++j) {
-              double s = Ar[tid][j];
-              for (int t = 0; t < j; ++t) s -= Ar[tid][t] * Lp[j][t];
-              Ar[tid][j] = s / Lp[j][j];
-            }
-          __syncthreads();
-          for (int e = tid; e < rw * pw; e += PO_T) {
-            int i = e % rw, j = e / rw;
-            A[(r0 + i) + (long long)(p0 + j) * n] = Ar[i][j];
-          }
+        __syncthreads();
+        for (int e = tid; e < rw * pw; e += PO_T) {
+          int i = e % rw, j = e / rw;
+          A[(r0 + i) + (long long)(p0 + j) * n] = Ar[i][j];
         }
       }
     }
-    // every CTA that factored A_pp agrees on failure; CTA p reports it
-    if (r == p && tid == 0 && fail >= 0) atomicCAS(info, -1, fail);
     grid.sync();
     if (*(volatile int*)info >= 0) break;
+    // ---- phase 2: trailing lower tiles (r, c), p < c <= r ------------------------
+    const int ntr = nt - p - 1;
+    const int ntiles = ntr * (ntr + 1) / 2;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      // t -> (rr, cc) with cc <= rr in the trailing triangle
+      int rr = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while (rr * (rr + 1) / 2 > t) --rr;
+      while ((rr + 1) * (rr + 2) / 2 <= t) ++rr;
+      int cc = t - rr * (rr + 1) / 2;
+      const int r = p + 1 + rr, c = p + 1 + cc;
+      const int r0 = r * PB, c0 = c * PB, rw = bw(r), cw = bw(c);
+      __syncthreads();
+      for (int e = tid; e < PB * PB; e += PO_T) {
+        int i = e % PB, k = e / PB;
+        Ar[i][k] = (i < rw && k < pw) ? A[(r0 + i) + (long long)(p0 + k) * n] : 0.0;
+        Lb[i][k] = (i < cw && k < pw) ? A[(c0 + i) + (long long)(p0 + k) * n] : 0.0;
+      }
+      __syncthreads();
+      const int ci = tid & 31, rj = tid >> 5;
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < PB; ++k) {
+        double bv = Lb[ci][k];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += Ar[rj + 4 * u][k] * bv;
+      }
+      if (ci < cw)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          int i = rj + 4 * u;
+          if (i < rw) A[(r0 + i) + (long long)(c0 + ci) * n] -= acc[u];
+        }
+    }
+    grid.sync();
   }
-  // zero the strict upper triangle of this row block (dense_kernels.cpp:79-80)
-  for (long long e = tid; e < (long long)rw * n; e += PO_T) {
-    int i = (int)(e % rw), j = (int)(e / rw);
-    if (r0 + i < j) A[(r0 + i) + (long long)j * n] = 0.0;
+  // zero the strict upper triangle (dense_kernels.cpp:79-80)
+  for (long long e = blockIdx.x * (long long)PO_T + tid; e < (long long)n * n;
+       e += (long long)gridDim.x * PO_T) {
+    int i = (int)(e % n), j = (int)(e / n);
+    if (i < j) A[e] = 0.0;
   }
 }
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
 
+static int coop_grid(const void* kernel, int threads, int want) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+  int cap = sms * (per > 0 ? per : 1);
+  return want < cap ? (want > 0 ? want : 1) : cap;
+}
+
 void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st) {
   (void)desc;
   set_int_kernel<<<1, 1, 0, st>>>(info, -1);
-  int nblk = (n + PB - 1) / PB;
+  int nt = (n + PB - 1) / PB;
+  int grid = coop_grid((const void*)potrf_coop_kernel, PO_T, std::max(nt, nt * (nt - 1) / 2));
   void* args[] = {&A, &n, &info};
-  TLRG_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel, dim3(nblk), dim3(PO_T), args, 0,
+  TLRG_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel, dim3(grid), dim3(PO_T), args, 0,
                                         st));
 }
 
@@ -360,65 +393,97 @@ void sytrf_bk(double* A, int n, double* d, double* e, uint8_t* s2, int* perm, in
 }
 
 // ----------------------------------------------------------------- TRSM ---
-// X = L^{-1} B for a panel of right-hand sides; one CTA per TR_C columns, X in
-// shared memory, L streamed through shared memory in 32 x 32 blocks.
-// LDL mode (perm != null): rows are gathered through perm, L is unit lower and
-// the block diagonal D^{-1} is applied last (factor.cpp:257-262).
-constexpr int TR_C = 8;
-constexpr int TR_T = 256;
+// X = L^{-1} B for the whole column panel (all tiles share L_kk), right-looking
+// over 32-row blocks in one cooperative kernel; 32 x 32 (row block, column
+// chunk) tiles are spread over a persistent grid.  Per block row p:
+//   phase 1: X_p <- L_pp^{-1} X_p       (warp-parallel substitution)  grid.sync
+//   phase 2: X_r -= L_rp X_p, r > p     (32^3 tile products)          grid.sync
+// LDL mode (perm != null): X = P B gathered first, L unit lower, D^{-1} applied
+// last (factor.cpp:257-262, dense_kernels.cpp:126-144).
+constexpr int TR_T = 128;
 
-__global__ void __launch_bounds__(TR_T) trsm_panel_kernel(const double* L, int n, double* B,
-                                                          long long nrhs, const int* perm,
-                                                          const double* d, const double* e,
-                                                          const uint8_t* s2, int* info) {
-  extern __shared__ double X[];  // n x TR_C, ld n
+__global__ void __launch_bounds__(TR_T) trsm_coop_kernel(const double* L, int n, double* B,
+                                                         long long nrhs, const int* perm,
+                                                         const double* d, const double* e,
+                                                         const uint8_t* s2, int* info,
+                                                         double* W) {
+  cg::grid_group grid = cg::this_grid();
   __shared__ double Ls[32][33];
-  const long long c0 = (long long)blockIdx.x * TR_C;
-  const int nc = (int)(nrhs - c0 < TR_C ? nrhs - c0 : TR_C);
+  __shared__ double Xs[32][33];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool unit = perm != nullptr;
-  for (int t = tid; t < n * TR_C; t += TR_T) {
-    int i = t % n, c = t / n;
-    int src = unit ? perm[i] : i;
-    X[i + c * n] = c < nc ? B[src + (c0 + c) * (long long)n] : 0.0;
+  const bool ldl = perm != nullptr;
+  double* X = ldl ? W : B;
+  const int nt = (n + 31) / 32;
+  const long long ncc = (nrhs + 31) / 32;
+  if (ldl) {
+    for (long long t = blockIdx.x * (long long)TR_T + tid; t < (long long)n * nrhs;
+         t += (long long)gridDim.x * TR_T) {
+      int i = (int)(t % n);
+      long long c = t / n;
+      X[t] = B[perm[i] + c * n];
+    }
+    grid.sync();
   }
-  __syncthreads();
-  const int ri = tid & 31, cc = tid >> 5;  // row in block, column (TR_C = 8 = warps)
-  for (int p0 = 0; p0 < n; p0 += 32) {
-    const int pw = min(32, n - p0);
-    // X_p -= L[p, 0:p0] X[0:p0]
-    double acc = 0.0;
-    for (int q0 = 0; q0 < p0; q0 += 32) {
+  for (int p = 0; p < nt; ++p) {
+    const int p0 = p * 32, pw = min(32, n - p0);
+    for (long long cc = blockIdx.x; cc < ncc; cc += gridDim.x) {
+      const long long c0 = cc * 32;
+      const int cw = (int)min(32LL, nrhs - c0);
+      __syncthreads();
       for (int t = tid; t < 32 * 32; t += TR_T) {
         int i = t % 32, k = t / 32;
-        Ls[i][k] = i < pw ? L[(p0 + i) + (long long)(q0 + k) * n] : 0.0;
+        Ls[i][k] = (i < pw && k < pw) ? L[(p0 + i) + (long long)(p0 + k) * n] : 0.0;
+        Xs[i][k] = (i < pw && k < cw) ? X[(p0 + i) + (c0 + k) * n] : 0.0;
       }
       __syncthreads();
-#pragma unroll 8
-      for (int k = 0; k < 32; ++k) acc += Ls[ri][k] * X[(q0 + k) + cc * n];
+      for (int c = warp; c < cw; c += TR_T / 32) {
+        double xi = Xs[lane][c];
+        for (int j = 0; j < pw; ++j) {
+          double xj = __shfl_sync(0xffffffffu, xi, j);
+          if (!ldl) xj /= Ls[j][j];
+          if (lane == j) xi = xj;
+          if (lane > j) xi -= Ls[lane][j] * xj;
+        }
+        if (lane < pw) X[(p0 + lane) + (c0 + c) * n] = xi;
+      }
+    }
+    grid.sync();
+    const long long ntiles = (long long)(nt - p - 1) * ncc;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int r = p + 1 + (int)(t / ncc);
+      const long long c0 = (t % ncc) * 32;
+      const int r0 = r * 32, rw = min(32, n - r0), cw = (int)min(32LL, nrhs - c0);
       __syncthreads();
+      for (int q = tid; q < 32 * 32; q += TR_T) {
+        int i = q % 32, k = q / 32;
+        Ls[i][k] = (i < rw && k < pw) ? L[(r0 + i) + (long long)(p0 + k) * n] : 0.0;
+        Xs[i][k] = (i < pw && k < cw) ? X[(p0 + i) + (c0 + k) * n] : 0.0;
+      }
+      __syncthreads();
+      const int ci = tid & 31, rj = tid >> 5;
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        double xv = Xs[k][ci];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += Ls[rj + 4 * u][k] * xv;
+      }
+      if (ci < cw)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          int i = rj + 4 * u;
+          if (i < rw) X[(r0 + i) + (c0 + ci) * n] -= acc[u];
+        }
     }
-    // diagonal block: load L_pp, then warp cc solves column cc (lane = row)
-    for (int t = tid; t < 32 * 32; t += TR_T) {
-      int i = t % 32, k = t / 32;
-      Ls[i][k] = (i < pw && k < pw) ? L[(p0 + i) + (long long)(p0 + k) * n] : 0.0;
-    }
-    __syncthreads();
-    double xi = ri < pw ? X[(p0 + ri) + cc * n] - acc : 0.0;
-    for (int j = 0; j < pw; ++j) {
-      double xj = __shfl_sync(0xffffffffu, xi, j);
-      if (!unit) xj /= Ls[j][j];
-      if (lane == j) xi = xj;
-      if (lane > j) xi -= Ls[lane][j] * xj;
-    }
-    if (ri < pw) X[(p0 + ri) + cc * n] = xi;
-    __syncthreads();
-    (void)warp;
+    grid.sync();
   }
-  if (unit && d) {
-    // D^{-1} (dense_kernels.cpp:126-144)
-    if (tid < nc) {
-      double* xc = X + tid * n;
+  if (ldl) {
+    // D^{-1} per column, then scatter back into B
+    for (long long c = blockIdx.x * (long long)TR_T + tid; c < nrhs;
+         c += (long long)gridDim.x * TR_T) {
+      double* xc = X + c * n;
       int k = 0;
       while (k < n) {
         if (s2[k]) {
@@ -441,24 +506,36 @@ __global__ void __launch_bounds__(TR_T) trsm_panel_kernel(const double* L, int n
         }
       }
     }
-    __syncthreads();
+    grid.sync();
+    for (long long t = blockIdx.x * (long long)TR_T + tid; t < (long long)n * nrhs;
+         t += (long long)gridDim.x * TR_T)
+      B[t] = X[t];
   }
-  for (int t = tid; t < n * nc; t += TR_T) {
-    int i = t % n, c = t / n;
-    B[i + (c0 + c) * (long long)n] = X[i + c * n];
+}
+
+static double* trsm_scratch(size_t n) {
+  static double* p = nullptr;
+  static size_t cap = 0;
+  if (n > cap) {
+    if (p) cudaFree(p);
+    TLRG_CUDA(cudaMalloc(&p, n * sizeof(double)));
+    cap = n;
   }
+  return p;
 }
 
 void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
                 const double* d, const double* e, const uint8_t* s2, int* info,
                 cudaStream_t st) {
-  static size_t lim = enable_max_dyn_smem(trsm_panel_kernel);
   if (nrhs <= 0 || n <= 0) return;
-  size_t bytes = (size_t)n * TR_C * 8;
-  if (bytes > lim) throw CudaError("trsm_panel: tile too large for shared memory");
-  unsigned blocks = (unsigned)((nrhs + TR_C - 1) / TR_C);
-  trsm_panel_kernel<<<blocks, TR_T, bytes, st>>>(L, n, B, nrhs, perm, d, e, s2, info);
-  TLRG_CUDA(cudaGetLastError());
+  double* W = perm ? trsm_scratch((size_t)n * nrhs) : nullptr;
+  const int nt = (n + 31) / 32;
+  const long long ncc = (nrhs + 31) / 32;
+  long long want = std::max<long long>(ncc, (long long)(nt - 1) * ncc);
+  int grid = coop_grid((const void*)trsm_coop_kernel, TR_T, (int)std::min<long long>(want, 1 << 20));
+  void* args[] = {&L, &n, &B, &nrhs, &perm, &d, &e, &s2, &info, &W};
+  TLRG_CUDA(cudaLaunchCooperativeKernel((void*)trsm_coop_kernel, dim3(grid), dim3(TR_T), args, 0,
+                                        st));
 }
 
 // -------------------------------------------------------------- HELPERS ---

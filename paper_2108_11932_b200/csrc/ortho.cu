@@ -83,6 +83,8 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   }
   __syncthreads();
   const double tiny2 = s_tiny;
+  // rotation threshold: rounding level of an m-term dot product (dgesvj style)
+  const double tol = fmax(1e-15, 2.0 * sqrt((double)m) * 2.220446049250313e-16);
   const int nn = n + (n & 1);
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) rotated = 0;
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
         al = warp_sum(al);
         be = warp_sum(be);
         ga = warp_sum(ga);
-        if (al > tiny2 && be > tiny2 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+        if (al > tiny2 && be > tiny2 && fabs(ga) > tol * sqrt(al * be)) {
           double zeta = (be - al) / (2.0 * ga);
           double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           double c = 1.0 / sqrt(1.0 + t * t), s = c * t;

@@ -192,12 +192,14 @@ __device__ void cta_generate(GaussStreams& G, int s, long long have, long long t
     }
     __syncthreads();
     const int chunk = S.chunk;
+    const long long base = have % G.cap;  // even, cap even: a pair never wraps apart
     for (int i = tid; i < chunk; i += blockDim.x) {
       double q = S.ps[i];
       double f = sqrt(-2.0 * log(q) / q);
-      long long p0 = have + 2 * i;  // even, cap even: the pair never wraps apart
-      buf[p0 % G.cap] = S.pu[i] * f;
-      buf[(p0 + 1) % G.cap] = S.pv[i] * f;
+      long long p0 = base + 2LL * i;
+      while (p0 >= G.cap) p0 -= G.cap;
+      buf[p0] = S.pu[i] * f;
+      buf[p0 + 1] = S.pv[i] * f;
     }
     have += 2LL * chunk;
     __syncthreads();
@@ -209,6 +211,15 @@ __device__ void cta_generate(GaussStreams& G, int s, long long have, long long t
     G.avail[s] = have;
   }
   __syncthreads();
+}
+
+// dst[0..n) <- ring[(pos + e) mod cap], without a per-element modulo
+__device__ __forceinline__ void ring_copy(const double* ring, long long cap, long long pos,
+                                          long long n, double* dst, int nthreads) {
+  const long long start = pos % cap;
+  const long long first = n < cap - start ? n : cap - start;
+  for (long long e = threadIdx.x; e < first; e += nthreads) dst[e] = ring[start + e];
+  for (long long e = first + threadIdx.x; e < n; e += nthreads) dst[e] = ring[e - first];
 }
 
 __device__ __forceinline__ long long ring_target(const GaussStreams& G, long long cur,
@@ -240,7 +251,7 @@ __global__ void __launch_bounds__(RT) gauss_round_kernel(GaussStreams G, const i
   const double* b = G.buf + (long long)s * G.cap;
   double* dst = Om + (long long)s * cols * bs;
   const long long n = (long long)cols * bs;
-  for (long long e = threadIdx.x; e < n; e += RT) dst[e] = b[(cur + e) % G.cap];
+  ring_copy(b, G.cap, cur, n, dst, RT);
   __syncthreads();
   if (threadIdx.x == 0) G.cursor[s] = cur + n;
 }
@@ -252,7 +263,7 @@ __global__ void __launch_bounds__(256) gauss_gather_kernel(GaussStreams G, const
   const long long c0 = G.cursor[s];
   const double* b = G.buf + (long long)s * G.cap;
   double* dst = out + (long long)blockIdx.x * out_stride;
-  for (long long e = threadIdx.x; e < count; e += 256) dst[e] = b[(c0 + e) % G.cap];
+  ring_copy(b, G.cap, c0, count, dst, 256);
   __syncthreads();
   if (threadIdx.x == 0) G.cursor[s] = c0 + count;
 }
@@ -459,8 +470,7 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
         rep_used = 0;
         rep_n = w - j;
         __syncthreads();
-        for (long long e = tid; e < (long long)rows * rep_n; e += PT)
-          T.rep[e] = T.gbuf[(c0 + e) % T.gcap];
+        ring_copy(T.gbuf, T.gcap, c0, (long long)rows * rep_n, T.rep, PT);
         __syncthreads();
         if (q > 0) {
           for (int pi = warp; pi < q * rep_n; pi += PW) {
