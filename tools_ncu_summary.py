@@ -7,7 +7,7 @@ for r in rows:
     name = r['Kernel Name'].split('(')[0]
     v = float(r['Metric Value'].replace(',', ''))
     u = r['Metric Unit']
-    v = v / 1000 if u == 'nsecond' else v * 1000 if u == 'msecond' else v
+    v = v / 1000 if u in ('nsecond', 'ns') else v * 1000 if u in ('msecond', 'ms') else v
     agg[name][0] += 1
     agg[name][1] += v
 tot = sum(a[1] for a in agg.values())
