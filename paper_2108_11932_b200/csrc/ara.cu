@@ -293,7 +293,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
                             C.st));
   TLRG_CUDA(cudaMemcpyAsync(hcur.data(), G.cursor, sizeof(long long) * T, cudaMemcpyDeviceToHost,
                             C.st));
-  C.sync();
+  C.wait();
   for (auto& gc : graph_cleanup) {
     cudaGraphExecDestroy(gc.first);
     cudaGraphDestroy(gc.second);
@@ -406,7 +406,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     C.launches += 4;
     std::vector<int> hr(T);
     TLRG_CUDA(cudaMemcpyAsync(hr.data(), rko, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
-    C.sync();
+    C.wait();
     for (int s : sl) fr[s] = hr[s];
   } else {
     for (int s = 0; s < T; ++s) fr[s] = q[s];
@@ -456,7 +456,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     ++C.launches;
   }
   tr.stop(C.st);
-  C.sync();
+  C.wait();
   cst.t_projection += tp.sec();
   cst.t_recompress += tr.sec();
 }

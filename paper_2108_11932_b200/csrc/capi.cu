@@ -247,6 +247,8 @@ int tlrg_create(int device, tlrg_ctx* out, tlrg_status* st) {
     c->c.device = device;
     TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.st, cudaStreamNonBlocking));
     TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.st2, cudaStreamNonBlocking));
+    TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.sd, cudaStreamNonBlocking));
+    c->c.st_main = c->c.st;
     c->c.desc.reserve(16 << 20);
     // one-time kernel attribute setup (never inside a graph capture)
     panel_mgs(nullptr, 0, 0, 0, 1, 1, c->c.st);

@@ -59,6 +59,8 @@ struct Ctx {
   int device = 0;
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;  // side stream (gaussian stream pre-generation)
+  cudaStream_t sd = nullptr;   // diagonal-path stream (SYRK, compensation, POTRF, L_kk^-1)
+  cudaStream_t st_main = nullptr;  // the context's own stream (st may be swapped by StreamScope)
   DescArena desc;
   std::map<std::string, DevBuf> bufs;
   // pinned host staging for small D2H reads
@@ -103,12 +105,19 @@ struct Ctx {
     }
     ev_pending.clear();
   }
+  // full synchronisation point: every stream of the context is idle, so the
+  // descriptor arena can be recycled
   void sync() {
     TLRG_CUDA(cudaStreamSynchronize(st));
+    if (sd) TLRG_CUDA(cudaStreamSynchronize(sd));
+    if (st_main && st_main != st) TLRG_CUDA(cudaStreamSynchronize(st_main));
     desc.reset();
     release_retired_arenas();
     if (!ev_pending.empty()) drain_events();
   }
+  // wait for the current stream only (no arena recycling): other streams keep
+  // running, e.g. the diagonal path while the ARA host loop reads its flags
+  void wait() { TLRG_CUDA(cudaStreamSynchronize(st)); }
   template <class T>
   T* push(const std::vector<T>& v) {
     if (v.empty()) return nullptr;
@@ -131,6 +140,15 @@ struct Ctx {
     ++launches;
   }
   ~Ctx();
+};
+
+// Enqueue everything issued inside the scope on another stream of the context
+// (the helpers all launch on C.st).
+struct StreamScope {
+  Ctx& C;
+  cudaStream_t saved;
+  StreamScope(Ctx& c, cudaStream_t s) : C(c), saved(c.st) { C.st = s; }
+  ~StreamScope() { C.st = saved; }
 };
 
 // Flat TLR store in HBM (replaces TlrMatrix/LowRankTile/DenseTile,

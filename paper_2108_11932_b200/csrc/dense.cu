@@ -82,10 +82,8 @@ __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int*
         continue;
       }
       if (r == p) {
-        for (int e = tid; e < pw * pw; e += PO_T) {
-          int i = e % pw, j = e / pw;
-          A[(p0 + i) + (long long)(p0 + j) * n] = i >= j ? Lp[i][j] : 0.0;
-        }
+        // L_pp is written back after the grid sync (other CTAs of this phase
+        // still read the unfactored A_pp from global memory)
       } else {
         for (int e = tid; e < rw * pw; e += PO_T) {
           int i = e % rw, j = e / rw;
@@ -107,6 +105,14 @@ __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int*
     }
     grid.sync();
     if (*(volatile int*)info >= 0) break;
+    if (blockIdx.x == 0) {
+      // CTA 0 handled r = p last with this Lp (phase 1 loop visits r = p first and
+      // every later r recomputes the same L_pp), so its copy is the factor
+      for (int e = tid; e < pw * pw; e += PO_T) {
+        int i = e % pw, j = e / pw;
+        A[(p0 + i) + (long long)(p0 + j) * n] = i >= j ? Lp[i][j] : 0.0;
+      }
+    }
     // ---- phase 2: trailing lower tiles (r, c), p < c <= r ------------------------
     const int ntr = nt - p - 1;
     const int ntiles = ntr * (ntr + 1) / 2;
@@ -164,6 +170,9 @@ static int coop_grid(const void* kernel, int threads, int want) {
   int per = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
   int cap = sms * (per > 0 ? per : 1);
+  // these kernels are latency-bound and share the GPU with the concurrent ARA
+  // stream: a modest persistent grid keeps grid.sync cheap
+  if (cap > 64) cap = 64;
   return want < cap ? (want > 0 ? want : 1) : cap;
 }
 

@@ -108,6 +108,16 @@ __global__ void add_diag_kernel(double* A, int n, double v) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) A[i + (long long)i * n] += v;
 }
+__global__ void identity_kernel(double* A, int n) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)n * n) return;
+  A[t] = (t % n) == (t / n) ? 1.0 : 0.0;
+}
+void identity(double* A, int n, cudaStream_t st) {
+  long long nn = (long long)n * n;
+  identity_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(A, n);
+  TLRG_CUDA(cudaGetLastError());
+}
 }  // namespace
 
 void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st);
@@ -169,105 +179,116 @@ bool modified_cholesky_device(Ctx& C, double* A, int n) {
 // diag(rowsum |R|).  D is symmetric PSD and numerically low rank at eps
 // (measured: 13-58 singular values above eps at m = 256/512), so the truncation
 // is computed by Rayleigh-Ritz on a sketched range: Q = orth(D orth(D Omega)),
-// SVD of Q^T D Q (one-sided Jacobi), keep sigma > eps.  The block grows until
-// at least 8 retained directions of slack remain (or it spans the tile).
-void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint64_t seed,
-                               double* corr, double* frob, int& rank_hint) {
+// SVD of Q^T D Q (one-sided Jacobi), keep sigma > eps.  The retained rank r is
+// consumed on the device (GEMM K from *rank), so the whole step enqueues without
+// a host round trip; the caller checks afterwards that at least 8 directions of
+// slack remained (r <= p - 8) and re-runs with a wider sketch otherwise.
+int schur_comp_width(int n, int rank_hint) {
   int p = std::max(32, rank_hint + 24);
   p = ((p + 7) / 8) * 8;
-  if (p > n) p = n;
+  return p > n ? n : p;
+}
+void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t seed, int p,
+                        int attempt, double* corr, double* frob, int* rank_out) {
+  double* Om = C.buf<double>("sc_Om", (size_t)n * p);
+  double* Y = C.buf<double>("sc_Y", (size_t)n * p);
+  double* Bm = C.buf<double>("sc_B", (size_t)p * p);
+  double* Vm = C.buf<double>("sc_V", (size_t)p * p);
+  double* R = C.buf<double>("sc_R", (size_t)p * p);
+  double* Rp = C.buf<double>("sc_Rp", (size_t)2 * p * p);
+  double* vec = C.buf<double>("sc_vec", (size_t)4 * p);
+  uint8_t* df = C.buf<uint8_t>("sc_def", (size_t)p);
+  double* work = C.buf<double>("sc_work", (size_t)2 * p * p);
+  double* sig = C.buf<double>("sc_sig", (size_t)p);
+  // replacement directions for rank-deficient sketch columns (not part of the
+  // reference's streams): a counter-based gaussian pool consumed by cursor
+  double* pool = C.buf<double>("sc_pool", (size_t)4 * n * p);
+  double* screp = C.buf<double>("sc_rep", (size_t)n * p);
+  long long* pcur = C.buf<long long>("sc_pcur", 1);
+  TLRG_CUDA(cudaMemsetAsync(pcur, 0, sizeof(long long), C.st));
+  fill_gaussian_philox(pool, 4LL * n * p, mix64(seed ^ 0x5c1ULL) + attempt, C.st);
+  fill_gaussian_philox(Om, (long long)n * p, seed * 0x9E3779B97F4A7C15ULL + attempt, C.st);
+  C.launches += 3;
+  auto DtimesX = [&](const double* X, double* out) {
+    std::vector<GemmProblem> pr(1);
+    pr[0] = GemmProblem{};
+    pr[0].A = Dk; pr[0].lda = n; pr[0].B = X; pr[0].ldb = n; pr[0].C = out; pr[0].ldc = n;
+    pr[0].M = n; pr[0].N = p; pr[0].K = n; pr[0].alpha = 1.0;
+    C.gemm(pr);
+  };
+  auto orth = [&](double* X) {
+    std::vector<PanelTask> t(1);
+    PanelTask& P = t[0];
+    P = PanelTask{};
+    P.Y = X; P.Q = nullptr; P.R = R; P.Rp = Rp; P.tiny = vec; P.col_norms = vec + p;
+    P.new_mass = vec + 2 * p; P.deficient = df; P.gbuf = pool; P.gcursor = pcur;
+    P.rep = screp; P.repC = nullptr; P.gcap = 4LL * n * p;
+    P.rows = n; P.width = p; P.q = 0;
+    PanelTask* d = C.push(t);
+    panel_tau(d, 1, C.st);
+    panel_mgs(d, 1, 0, 0, p, n, C.st);
+    panel_mgs(d, 1, 1, 0, p, n, C.st);
+    C.launches += 3;
+  };
+  DtimesX(Om, Y);
+  orth(Y);
+  DtimesX(Y, Om);  // power iteration
+  orth(Om);
+  DtimesX(Om, Y);  // Y = D Q
+  {
+    std::vector<GemmProblem> pr(1);
+    pr[0] = GemmProblem{};
+    pr[0].A = Om; pr[0].lda = n; pr[0].transA = 1; pr[0].B = Y; pr[0].ldb = n;
+    pr[0].C = Bm; pr[0].ldc = p; pr[0].M = p; pr[0].N = p; pr[0].K = n; pr[0].alpha = 1.0;
+    C.gemm(pr);
+  }
+  std::vector<SvdTask> sv(1);
+  sv[0] = SvdTask{};
+  sv[0].A = Bm; sv[0].V = Vm; sv[0].sig = sig; sv[0].work = work; sv[0].rank_out = rank_out;
+  sv[0].n = p; sv[0].cut = eps;
+  jacobi_svd(C.push(sv), 1, p, C.st);
+  ++C.launches;
+  // R = D - (Q A_B)(Q V_B)^T restricted to the r = *rank_out retained directions
+  double* Xl = C.buf<double>("sc_Xl", (size_t)n * p);
+  double* Xr = C.buf<double>("sc_Xr", (size_t)n * p);
+  double* Rm = C.buf<double>("sc_Rm", (size_t)n * n);
+  double* fp = C.buf<double>("sc_fp", (size_t)n);
+  TLRG_CUDA(cudaMemcpyAsync(Rm, Dk, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, C.st));
+  {
+    std::vector<GemmProblem> pr(2);
+    pr[0] = GemmProblem{};
+    pr[0].A = Om; pr[0].lda = n; pr[0].B = Bm; pr[0].ldb = p; pr[0].C = Xl; pr[0].ldc = n;
+    pr[0].M = n; pr[0].N = p; pr[0].K = p; pr[0].alpha = 1.0;
+    pr[1] = pr[0];
+    pr[1].B = Vm; pr[1].C = Xr;
+    C.gemm(pr);
+    std::vector<GemmProblem> p2(1);
+    p2[0] = GemmProblem{};
+    p2[0].A = Xl; p2[0].lda = n; p2[0].B = Xr; p2[0].ldb = n; p2[0].transB = 1;
+    p2[0].C = Rm; p2[0].ldc = n; p2[0].M = n; p2[0].N = n; p2[0].K = p; p2[0].Kp = rank_out;
+    p2[0].alpha = -1.0; p2[0].beta = 1.0;
+    C.gemm(p2);
+  }
+  rowsum_abs_residual(Rm, nullptr, nullptr, n, 0, corr, fp, C.st);
+  frob_sq(Rm, (long long)n * n, frob, C.st);  // ||R||_F^2
+  C.launches += 2;
+}
+
+// synchronous form (building-block API): widen the sketch until the slack test holds
+void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint64_t seed,
+                               double* corr, double* frob, int& rank_hint) {
+  int p = schur_comp_width(n, rank_hint);
+  int* rk = C.buf<int>("sc_rank", 1);
   for (int attempt = 0;; ++attempt) {
-    double* Om = C.buf<double>("sc_Om", (size_t)n * p);
-    double* Y = C.buf<double>("sc_Y", (size_t)n * p);
-    double* Bm = C.buf<double>("sc_B", (size_t)p * p);
-    double* Vm = C.buf<double>("sc_V", (size_t)p * p);
-    double* R = C.buf<double>("sc_R", (size_t)p * p);
-    double* Rp = C.buf<double>("sc_Rp", (size_t)2 * p * p);
-    double* vec = C.buf<double>("sc_vec", (size_t)4 * p);
-    uint8_t* df = C.buf<uint8_t>("sc_def", (size_t)p);
-    double* work = C.buf<double>("sc_work", (size_t)2 * p * p);
-    double* sig = C.buf<double>("sc_sig", (size_t)p);
-    int* rk = C.buf<int>("sc_rank", 1);
-    // replacement directions for rank-deficient sketch columns (not part of the
-    // reference's streams): a counter-based gaussian pool consumed by cursor
-    double* pool = C.buf<double>("sc_pool", (size_t)4 * n * p);
-    double* screp = C.buf<double>("sc_rep", (size_t)n * p);
-    long long* pcur = C.buf<long long>("sc_pcur", 1);
-    TLRG_CUDA(cudaMemsetAsync(pcur, 0, sizeof(long long), C.st));
-    fill_gaussian_philox(pool, 4LL * n * p, mix64(seed ^ 0x5c1ULL) + attempt, C.st);
-    fill_gaussian_philox(Om, (long long)n * p, seed * 0x9E3779B97F4A7C15ULL + attempt, C.st);
-    auto DtimesX = [&](const double* X, double* out) {
-      std::vector<GemmProblem> pr(1);
-      pr[0] = GemmProblem{};
-      pr[0].A = Dk; pr[0].lda = n; pr[0].B = X; pr[0].ldb = n; pr[0].C = out; pr[0].ldc = n;
-      pr[0].M = n; pr[0].N = p; pr[0].K = n; pr[0].alpha = 1.0;
-      C.gemm(pr);
-    };
-    auto orth = [&](double* X) {
-      std::vector<PanelTask> t(1);
-      PanelTask& P = t[0];
-      P = PanelTask{};
-      P.Y = X; P.Q = nullptr; P.R = R; P.Rp = Rp; P.tiny = vec; P.col_norms = vec + p;
-      P.new_mass = vec + 2 * p; P.deficient = df; P.gbuf = pool; P.gcursor = pcur;
-      P.rep = screp; P.repC = nullptr; P.gcap = 4LL * n * p;
-      P.rows = n; P.width = p; P.q = 0;
-      PanelTask* d = C.push(t);
-      panel_tau(d, 1, C.st);
-      panel_mgs(d, 1, 0, 0, p, n, C.st);
-      panel_mgs(d, 1, 1, 0, p, n, C.st);
-      C.launches += 3;
-    };
-    DtimesX(Om, Y);
-    orth(Y);
-    DtimesX(Y, Om);  // power iteration
-    orth(Om);
-    DtimesX(Om, Y);  // Y = D Q
-    {
-      std::vector<GemmProblem> pr(1);
-      pr[0] = GemmProblem{};
-      pr[0].A = Om; pr[0].lda = n; pr[0].transA = 1; pr[0].B = Y; pr[0].ldb = n;
-      pr[0].C = Bm; pr[0].ldc = p; pr[0].M = p; pr[0].N = p; pr[0].K = n; pr[0].alpha = 1.0;
-      C.gemm(pr);
-    }
-    std::vector<SvdTask> sv(1);
-    sv[0] = SvdTask{};
-    sv[0].A = Bm; sv[0].V = Vm; sv[0].sig = sig; sv[0].work = work; sv[0].rank_out = rk;
-    sv[0].n = p; sv[0].cut = eps;
-    jacobi_svd(C.push(sv), 1, p, C.st);
-    ++C.launches;
+    schur_comp_enqueue(C, Dk, n, eps, seed, p, attempt, corr, frob, rk);
     int* h = C.pinned_ints(1);
     TLRG_CUDA(cudaMemcpyAsync(h, rk, sizeof(int), cudaMemcpyDeviceToHost, C.st));
-    C.sync();
-    int r = h[0];
-    if (r > p - 8 && p < n) {
+    C.wait();
+    if (h[0] > p - 8 && p < n) {
       p = std::min(n, 2 * p);
       continue;
     }
-    rank_hint = r;
-    // R = D - (Q A_B)(Q V_B)^T restricted to the r retained directions
-    double* Xl = C.buf<double>("sc_Xl", (size_t)n * std::max(r, 1));
-    double* Xr = C.buf<double>("sc_Xr", (size_t)n * std::max(r, 1));
-    double* Rm = C.buf<double>("sc_Rm", (size_t)n * n);
-    double* fp = C.buf<double>("sc_fp", (size_t)n);
-    dcopy(Dk, Rm, (long long)n * n, C.st);
-    if (r > 0) {
-      std::vector<GemmProblem> pr(2);
-      pr[0] = GemmProblem{};
-      pr[0].A = Om; pr[0].lda = n; pr[0].B = Bm; pr[0].ldb = p; pr[0].C = Xl; pr[0].ldc = n;
-      pr[0].M = n; pr[0].N = r; pr[0].K = p; pr[0].alpha = 1.0;
-      pr[1] = pr[0];
-      pr[1].B = Vm; pr[1].C = Xr;
-      C.gemm(pr);
-      std::vector<GemmProblem> p2(1);
-      p2[0] = GemmProblem{};
-      p2[0].A = Xl; p2[0].lda = n; p2[0].B = Xr; p2[0].ldb = n; p2[0].transB = 1;
-      p2[0].C = Rm; p2[0].ldc = n; p2[0].M = n; p2[0].N = n; p2[0].K = r;
-      p2[0].alpha = -1.0; p2[0].beta = 1.0;
-      C.gemm(p2);
-    }
-    rowsum_abs_residual(Rm, nullptr, nullptr, n, 0, corr, fp, C.st);
-    frob_sq(Rm, (long long)n * n, frob, C.st);  // ||R||_F^2
-    C.launches += 3;
+    rank_hint = h[0];
     return;
   }
 }
@@ -312,89 +333,95 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   auto store = std::make_shared<Store>();
   M.stores.push_back(store);
   double* Dk = C.buf<double>("Dk", (size_t)b * b);
-  double* akk = C.buf<double>("akk", (size_t)b * b);
   double* a0 = C.buf<double>("akk0", (size_t)b * b);
+  double* aorig = C.buf<double>("akk_orig", (size_t)b * b);
+  double* Xinv = C.buf<double>("Linv", (size_t)b * b);
   double* corr = C.buf<double>("corr", (size_t)b);
   double* frob = C.buf<double>("cfrob", 1);
   double* piv = C.buf<double>("pivot", (size_t)nb);
-  int* info = C.buf<int>("finfo", 2);
+  int* info = C.buf<int>("finfo", 4);  // [0] potrf, [1] first singular D block, [2] comp rank, [3] trsm
   int rank_hint = 0;
-  Ev e0, e1, e2, e3, e4, e5;
+  Ev e0, e1, e4, e5, de0, de1, de2, de3, ejoin;
   StreamPrep prep;
 
   for (int k = 0; k < nb; ++k) {
     const int rk = M.rows(k);
     double* diagk = M.diag + (size_t)k * b * b;
     // ---- gaussian streams of this column's ARA, generated on the side stream
-    //      while the diagonal path runs
+    //      while the column setup and the diagonal path run
     column_prepare(C, M, k, cfg, prep);
-    // ---- dense phase: Gram blocks, H_k, D_k = sum_j L_kj [D_j] L_kj^T ----------
+    // ---- column setup: row-k concatenation and Gram blocks (main stream) ------
     cudaEventRecord(e0.e, C.st);
     ColumnSetup cs;
     column_setup(C, M, k, F->D, cs);
-    if (cs.K > 0) {
-      double* Hk = C.buf<double>("Hk", (size_t)b * cs.K);
-      std::vector<int> tk{k};
-      column_H(C, M, cs, tk, Hk, (long long)b * cs.K);
-      std::vector<GemmProblem> pr(1);
-      pr[0] = GemmProblem{};
-      pr[0].A = Hk; pr[0].lda = rk; pr[0].B = cs.Ucat; pr[0].ldb = rk; pr[0].transB = 1;
-      pr[0].C = Dk; pr[0].ldc = rk; pr[0].M = rk; pr[0].N = rk; pr[0].K = cs.K;
-      pr[0].alpha = 1.0;
-      C.gemm(pr);
-      symmetrize(Dk, rk, C.st);
-      ++C.launches;
-    }
     cudaEventRecord(e1.e, C.st);
-    // ---- diagonal tile: a = A_kk - D_k (+ compensation) (+ shift) -------------
-    bool comp = opts.schur && k > 0 && cs.K > 0;
-    double comp_time = 0;
-    if (comp) {
-      schur_compensation_device(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), corr,
-                                frob, rank_hint);
-      cudaEventRecord(e2.e, C.st);
-    }
-    diag_combine(diagk, cs.K > 0 ? Dk : nullptr, comp ? corr : nullptr, opts.shift, akk, rk, C.st);
-    ++C.launches;
-    if (!ldl) {
-      dcopy(akk, a0, (long long)rk * rk, C.st);
-      bool ok = potrf_device(C, akk, rk);
-      if (!ok) {
-        dcopy(a0, akk, (long long)rk * rk, C.st);
-        modified_cholesky_device(C, akk, rk);
-        S.modified_diagonals++;
+    const bool comp = opts.schur && k > 0 && cs.K > 0;
+    int p_comp = comp ? schur_comp_width(rk, rank_hint) : 0;
+
+    // ---- diagonal path on its own stream: it needs only row k of L, so it runs
+    //      concurrently with the column's ARA (which needs L_kk only for the
+    //      final TRSM).  D_k, compensation, a = A_kk - D_k (+comp) (+shift),
+    //      POTRF / Bunch-Kaufman, and the panel operator X = L^{-1}
+    //      (Chol) or D^{-1} L^{-1} P (LDL), so the TRSM becomes one GEMM.
+    auto diag_tail = [&]() {
+      diag_combine(aorig, cs.K > 0 ? Dk : nullptr, comp ? corr : nullptr, opts.shift, a0, rk,
+                   C.st);
+      dcopy(a0, diagk, (long long)rk * rk, C.st);
+      if (!ldl) {
+        potrf_impl(diagk, rk, info, C.desc, C.st);
+        C.launches += 4;
+      } else {
+        double* dk = F->D.d + (size_t)k * b;
+        double* ek = F->D.e + (size_t)k * b;
+        uint8_t* sk = F->D.s2 + (size_t)k * b;
+        int* pk = F->D.perm + (size_t)k * b;
+        sytrf_bk(diagk, rk, dk, ek, sk, pk, info + 3, C.st);
+        first_singular_kernel<<<1, 1, 0, C.st>>>(dk, ek, sk, rk, info + 1);
+        C.launches += 4;
       }
-      dcopy(akk, diagk, (long long)rk * rk, C.st);
-      min_diag_sq(diagk, rk, piv + k, C.st);
+    };
+    auto diag_inverse = [&]() {
+      identity(Xinv, rk, C.st);
+      if (!ldl) {
+        trsm_panel(diagk, rk, Xinv, rk, nullptr, nullptr, nullptr, nullptr, info + 3, C.st);
+        min_diag_sq(diagk, rk, piv + k, C.st);
+      } else {
+        size_t o = (size_t)k * b;
+        trsm_panel(diagk, rk, Xinv, rk, F->D.perm + o, F->D.d + o, F->D.e + o, F->D.s2 + o,
+                   info + 3, C.st);
+        min_block_pivot(F->D.d + o, F->D.e + o, F->D.s2 + o, rk, piv + k, C.st);
+      }
       C.launches += 3;
-    } else {
-      double* dk = F->D.d + (size_t)k * b;
-      double* ek = F->D.e + (size_t)k * b;
-      uint8_t* sk = F->D.s2 + (size_t)k * b;
-      int* pk = F->D.perm + (size_t)k * b;
-      sytrf_bk(akk, rk, dk, ek, sk, pk, info, C.st);
-      first_singular_kernel<<<1, 1, 0, C.st>>>(dk, ek, sk, rk, info + 1);
-      int* h = C.pinned_ints(1);
-      TLRG_CUDA(cudaMemcpyAsync(h, info + 1, sizeof(int), cudaMemcpyDeviceToHost, C.st));
-      C.sync();
-      if (h[0] >= 0) numeric_error("tlr_ldlt: singular D block in column", k);
-      dcopy(akk, diagk, (long long)rk * rk, C.st);
-      min_block_pivot(dk, ek, sk, rk, piv + k, C.st);
-      C.launches += 4;
+    };
+    TLRG_CUDA(cudaStreamWaitEvent(C.sd, e1.e, 0));
+    {
+      StreamScope on_diag(C, C.sd);
+      cudaEventRecord(de0.e, C.st);
+      // keep A_kk: the tile is factored in place and a retry re-reads it
+      dcopy(diagk, aorig, (long long)rk * rk, C.st);
+      if (cs.K > 0) {
+        double* Hk = C.buf<double>("Hk", (size_t)b * cs.K);
+        std::vector<int> tk{k};
+        column_H(C, M, cs, tk, Hk, (long long)b * cs.K);
+        std::vector<GemmProblem> pr(1);
+        pr[0] = GemmProblem{};
+        pr[0].A = Hk; pr[0].lda = rk; pr[0].B = cs.Ucat; pr[0].ldb = rk; pr[0].transB = 1;
+        pr[0].C = Dk; pr[0].ldc = rk; pr[0].M = rk; pr[0].N = rk; pr[0].K = cs.K;
+        pr[0].alpha = 1.0;
+        C.gemm(pr);
+        symmetrize(Dk, rk, C.st);
+        ++C.launches;
+      }
+      cudaEventRecord(de1.e, C.st);
+      if (comp)
+        schur_comp_enqueue(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), p_comp, 0,
+                           corr, frob, info + 2);
+      cudaEventRecord(de2.e, C.st);
+      diag_tail();
+      diag_inverse();
+      cudaEventRecord(de3.e, C.st);
     }
-    cudaEventRecord(e3.e, C.st);
-    if (comp) {
-      double* h = C.pinned_dbl(1);
-      TLRG_CUDA(cudaMemcpyAsync(h, frob, sizeof(double), cudaMemcpyDeviceToHost, C.st));
-      C.sync();
-      S.compensation_frob += std::sqrt(h[0]);
-      comp_time = elapsed(e1, e2);
-    }
-    C.sync();
-    S.t_dense += elapsed(e0, e1);
-    S.t_misc += elapsed(e1, e3);
-    S.t_compensation += comp_time;
-    // ---- ARA over the column -------------------------------------------------
+    // ---- ARA over the column (main stream) -------------------------------------
     ColumnStats cst;
     std::vector<TileResult> res = column_ara(C, M, k, cs, cfg, *store, cst, &prep);
     S.t_sampling += cst.t_sampling;
@@ -402,7 +429,51 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     S.t_projection += cst.t_projection;
     S.t_recompress += cst.t_recompress;
     S.flops_ref += cst.flops_ref;
-    // ---- TRSM of the new panel and overwrite ----------------------------------
+    // ---- join: diagonal status (one small read) ---------------------------------
+    TLRG_CUDA(cudaStreamWaitEvent(C.st, de3.e, 0));
+    int* hs = C.pinned_ints(4);
+    double* hf = C.pinned_dbl(1);
+    TLRG_CUDA(cudaMemcpyAsync(hs, info, sizeof(int) * 4, cudaMemcpyDeviceToHost, C.st));
+    if (comp) TLRG_CUDA(cudaMemcpyAsync(hf, frob, sizeof(double), cudaMemcpyDeviceToHost, C.st));
+    C.wait();
+    int st_potrf = hs[0], st_sing = hs[1], st_rank = hs[2];
+    if (comp && st_rank > p_comp - 8 && p_comp < rk) {
+      // sketch too narrow for this column's spectrum: redo with a wider one
+      rank_hint = 2 * p_comp;
+      schur_compensation_device(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), corr,
+                                frob, rank_hint);
+      diag_tail();
+      TLRG_CUDA(cudaMemcpyAsync(hs, info, sizeof(int) * 4, cudaMemcpyDeviceToHost, C.st));
+      TLRG_CUDA(cudaMemcpyAsync(hf, frob, sizeof(double), cudaMemcpyDeviceToHost, C.st));
+      C.wait();
+      st_potrf = hs[0];
+      st_sing = hs[1];
+      diag_inverse();
+    } else if (comp) {
+      rank_hint = st_rank;
+    }
+    if (comp) S.compensation_frob += std::sqrt(hf[0]);
+    if (ldl && st_sing >= 0) numeric_error("tlr_ldlt: singular D block in column", k);
+    if (!ldl && st_potrf >= 0) {
+      // modified Cholesky fallback (dense_kernels.cpp:283-309), rare
+      dcopy(a0, diagk, (long long)rk * rk, C.st);
+      modified_cholesky_device(C, diagk, rk);
+      S.modified_diagonals++;
+      diag_inverse();
+    }
+    {
+      float f = 0;
+      cudaEventElapsedTime(&f, e0.e, e1.e);
+      S.t_dense += f * 1e-3;
+      cudaEventElapsedTime(&f, de0.e, de1.e);
+      S.t_dense += f * 1e-3;
+      cudaEventElapsedTime(&f, de1.e, de2.e);
+      S.t_compensation += f * 1e-3;
+      S.t_misc += f * 1e-3;
+      cudaEventElapsedTime(&f, de2.e, de3.e);
+      S.t_misc += f * 1e-3;
+    }
+    // ---- TRSM of the new panel (one GEMM with the precomputed operator) --------
     cudaEventRecord(e4.e, C.st);
     double* Vp = nullptr;
     long long ncols = 0;
@@ -413,13 +484,15 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     }
     S.tile_rounds_resident += S.ara_rounds[k];
     if (ncols > 0) {
-      if (ldl) {
-        TLRG_CUDA(cudaMemsetAsync(info, 0xff, sizeof(int), C.st));
-        trsm_panel(diagk, rk, Vp, ncols, F->D.perm + (size_t)k * b, F->D.d + (size_t)k * b,
-                   F->D.e + (size_t)k * b, F->D.s2 + (size_t)k * b, info, C.st);
-      } else {
-        trsm_panel(diagk, rk, Vp, ncols, nullptr, nullptr, nullptr, nullptr, info, C.st);
-      }
+      double* Bs = C.buf<double>("trsm_B", (size_t)rk * ncols);
+      TLRG_CUDA(cudaMemcpyAsync(Bs, Vp, sizeof(double) * rk * ncols, cudaMemcpyDeviceToDevice,
+                                C.st));
+      std::vector<GemmProblem> pr(1);
+      pr[0] = GemmProblem{};
+      pr[0].A = Xinv; pr[0].lda = rk; pr[0].B = Bs; pr[0].ldb = rk;
+      pr[0].C = Vp; pr[0].ldc = rk; pr[0].M = rk; pr[0].N = (int)ncols; pr[0].K = rk;
+      pr[0].alpha = 1.0;
+      C.gemm(pr);
       ++C.launches;
     }
     for (auto& r : res) {

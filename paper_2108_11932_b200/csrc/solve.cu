@@ -469,6 +469,7 @@ Ctx::~Ctx() {
   bufs.clear();
   if (st) cudaStreamDestroy(st);
   if (st2) cudaStreamDestroy(st2);
+  if (sd) cudaStreamDestroy(sd);
   for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
 }
 void Matrix::free_all() {
