@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtlrg.so")
+LIB_PATH = os.environ.get("TLRG_LIB") or os.path.join(HERE, "lib", "libtlrg.so")
 
 dp = C.POINTER(C.c_double)
 ip = C.POINTER(C.c_int32)

@@ -169,6 +169,61 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     TLRG_CUDA(cudaMemcpyAsync(d_rows, S.rows.data(), sizeof(int) * T, cudaMemcpyHostToDevice,
                               C.st));
   }
+  const char* nf = std::getenv("TLRG_NO_FUSED");
+  const bool use_fused = op.fused.on && !(nf && nf[0] == '1') &&
+                         ara_fused_supported(maxrows, bs, window);
+  int capall = 0;
+  for (int s = 0; s < T; ++s) capall = std::max(capall, S.cap[s]);
+  const int max_rounds = 4 * capall + 8;  // a tile gains >= 1 column per round or converges
+  Timer tm;
+  std::vector<std::pair<cudaGraphExec_t, cudaGraph_t>> graph_cleanup;
+  if (use_fused) {
+    // ---- every round of every tile in ONE launch (one CTA per tile) ----------
+    tm.start(C.st);
+    const AraFusedOp& fo = op.fused;
+    long long wtot = 0;
+    std::vector<long long> woff(T);
+    for (int s = 0; s < T; ++s) {
+      woff[s] = wtot;
+      wtot += (long long)((fo.Ad.empty() || !fo.Ad[s] ? fo.kA[s] + fo.K : 0) + 1) * bs;
+    }
+    double* Wb = C.buf<double>("fusedW", (size_t)wtot);
+    double* rc = C.buf<double>("fusedRC", (size_t)T * capmax);
+    std::vector<FusedSlot> slots(T);
+    for (int s = 0; s < T; ++s) {
+      FusedSlot& f = slots[s];
+      f = FusedSlot{};
+      f.UA = fo.UA.empty() ? nullptr : fo.UA[s];
+      f.VA = fo.VA.empty() ? nullptr : fo.VA[s];
+      f.H = fo.H.empty() ? nullptr : fo.H[s];
+      f.kA = fo.kA.empty() ? 0 : fo.kA[s];
+      f.Ad = fo.Ad.empty() ? nullptr : fo.Ad[s];
+      f.ldad = fo.ldad.empty() ? 0 : fo.ldad[s];
+      f.rows = S.rows[s];
+      f.cap = S.cap[s];
+      f.Q = Q + s * Qstride;
+      f.Om = Om + (size_t)s * cols * bs;
+      f.W = Wb + woff[s];
+      f.Cq = Cdef + (size_t)s * capmax * bs;
+      f.repC = rc + (size_t)s * capmax;
+    }
+    FusedArgs fa{};
+    fa.slots = C.push(slots);
+    fa.G = G;
+    fa.Ucat = fo.Ucat;
+    fa.K = fo.K;
+    fa.cols = cols;
+    fa.bs = bs;
+    fa.window = window;
+    fa.max_rounds = max_rounds;
+    fa.eps = cfg.eps;
+    fa.eta = cfg.safety;
+    fa.qcols = qcols;
+    fa.rounds = rounds;
+    fa.conv = conv;
+    ara_fused(fa, T, maxrows, C.st);
+    ++C.launches;
+  } else {
   // ---- static per-column launch tables (staged before capture) ---------------
   std::vector<std::vector<GemmProblem>> stages;
   op.sample_plan(Om, Y, Ystride, done, stages);
@@ -230,14 +285,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     P.eta = cfg.safety;
   }
   PanelTask* d_tasks = C.push(tasks);
-  int capall = 0;
-  for (int s = 0; s < T; ++s) capall = std::max(capall, S.cap[s]);
-  const int max_rounds = 4 * capall + 8;  // a tile gains >= 1 column per round or converges
-
   // ---- the round loop: one CUDA graph, conditional WHILE node on device ------
-  Timer tm;
   tm.start(C.st);
-  std::vector<std::pair<cudaGraphExec_t, cudaGraph_t>> graph_cleanup;
   auto enqueue_round = [&]() {
     gauss_round(G, done, d_rows, T, cols, bs, Om, C.st);
     for (auto& pl : sample_plans) gemm_launch(pl, C.st);
@@ -282,6 +331,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     TLRG_CUDA(cudaGraphLaunch(exec, C.st));
     graph_cleanup.push_back({exec, graph});
   }
+  }
   tm.stop(C.st);
   std::vector<int> hq(T), h_rounds(T), h_conv(T), hact(2);
   std::vector<long long> hav(T), hcur(T);
@@ -298,8 +348,14 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     cudaGraphExecDestroy(gc.first);
     cudaGraphDestroy(gc.second);
   }
-  if (hact[0] > 0) throw CudaError("ara_batch: round limit reached with tiles still resident");
-  C.launches += (long long)hact[1] * (4 + (long long)sample_plans.size() + 6);
+  if (use_fused) {
+    for (int s = 0; s < T; ++s)
+      if (!h_conv[s] && hq[s] < S.cap[s])
+        throw CudaError("ara_batch: round limit reached with tiles still resident");
+  } else {
+    if (hact[0] > 0) throw CudaError("ara_batch: round limit reached with tiles still resident");
+    C.launches += (long long)hact[1] * 16;
+  }
   cst.t_sampling += tm.sec();  // the fused round loop (draws, sampling, orthog, absorb)
   for (int s = 0; s < T; ++s) {
     q[s] = hq[s];

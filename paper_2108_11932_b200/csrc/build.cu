@@ -179,6 +179,11 @@ std::unique_ptr<Matrix> build_tlr_device(Ctx& C, int dim, int64_t n, const doubl
       }
       C.gemm(pr);
     };
+    op.fused.on = true;
+    for (int s = 0; s < T; ++s) {
+      op.fused.Ad.push_back(D + (size_t)s * b * b);
+      op.fused.ldad.push_back(sl.rows[s]);
+    }
     std::vector<int> order(T);
     for (int s = 0; s < T; ++s) order[s] = s;
     AraOut out;

@@ -325,6 +325,17 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
       C.gemm(pr);
     }
   };
+  // the same operator in the fused kernel's form
+  op.fused.on = true;
+  op.fused.Ucat = cs.Ucat;
+  op.fused.K = K;
+  for (int s = 0; s < T; ++s) {
+    const long long t = M.t(queue[s], k);
+    op.fused.UA.push_back(kA[s] ? M.U[t] : nullptr);
+    op.fused.VA.push_back(kA[s] ? M.V[t] : nullptr);
+    op.fused.kA.push_back(kA[s]);
+    op.fused.H.push_back(K ? H + s * Hstride : nullptr);
+  }
   // results land in one panel ordered by ascending i (keeps V panels contiguous)
   std::vector<int> slot_of(nb, -1);
   for (int s = 0; s < T; ++s) slot_of[queue[s]] = s;

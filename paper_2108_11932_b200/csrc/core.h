@@ -230,7 +230,17 @@ struct AraSlots {
   std::vector<double> Sref;  // reference flops per sampled vector (optional)
   int cols = 0;
 };
+// Operator in the fused kernel's form (ara_fused.cu); optional.
+struct AraFusedOp {
+  bool on = false;
+  std::vector<const double*> UA, VA, H, Ad;
+  std::vector<int> kA;
+  std::vector<long long> ldad;
+  const double* Ucat = nullptr;
+  int K = 0;
+};
 struct AraOperator {
+  AraFusedOp fused;
   // GEMM stages computing Y_s = E_s Omega_s for every slot s (Omega_s at
   // Om + s*cols*bs, Y_s at Y + s*Ystride); each problem must carry
   // skip = done + s so converged tiles cost nothing in later rounds

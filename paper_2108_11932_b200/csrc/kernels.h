@@ -158,6 +158,40 @@ struct CopyItem {
 };
 void batched_copy(CopyItem* d_items, int n, cudaStream_t st);
 
+// ------------------------------------------------------------ FUSED ARA ---
+// One CTA per tile runs the whole adaptive loop (ara_fused.cu).
+struct FusedSlot {
+  // low-rank chain operator: Y = U^A (V^A^T Om) - H (Ucat^T Om)
+  const double* UA;   // rows x kA (ld rows)
+  const double* VA;   // cols x kA (ld cols)
+  const double* H;    // rows x K  (ld rows)
+  int kA;
+  // dense operator (build_tlr's DenseSampler): Y = Ad Om when Ad != null
+  const double* Ad;
+  long long ldad;
+  int rows, cap;
+  double* Q;     // rows x cap basis (ld rows), output
+  double* Om;    // cols x bs scratch
+  double* W;     // (kA + K) x bs scratch
+  double* Cq;    // cap x bs scratch
+  double* repC;  // cap scratch
+};
+struct FusedArgs {
+  const FusedSlot* slots;
+  GaussStreams G;
+  const double* Ucat;  // cols x K (ld cols), shared by all slots
+  int K, cols, bs, window, max_rounds;
+  double eps, eta;
+  int* qcols;
+  int* rounds;
+  int* conv;
+  int ldy;          // set by the launcher
+  long long ysz;    // set by the launcher
+  long long stg_half;  // set by the launcher
+};
+bool ara_fused_supported(int maxrows, int bs, int window);
+void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st);
+
 // ---------------------------------------------------------------- DENSE ---
 // Cholesky of an m x m tile in place (lower); info[0] = failing column or -1.
 void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st);

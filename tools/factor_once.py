@@ -1,6 +1,6 @@
 """Dev tool: build one config on the device and factor it once (for ncu)."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2108_11932_b200 as tg
 from paper_2108_11932_b200.tlr import build_tlr
 import bench

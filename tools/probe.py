@@ -1,6 +1,6 @@
 """Probe: build + factor one config on the GPU and print phases (dev tool)."""
 import sys, time, json, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2108_11932_b200 as tg
 from paper_2108_11932_b200.tlr import build_tlr
