@@ -170,7 +170,9 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
                               C.st));
   }
   const char* nf = std::getenv("TLRG_NO_FUSED");
-  const bool use_fused = op.fused.on && !(nf && nf[0] == '1') &&
+  bool even = (cols % 2) == 0;
+  for (int s = 0; s < T; ++s) even = even && (S.rows[s] % 2) == 0;
+  const bool use_fused = op.fused.on && !(nf && nf[0] == '1') && even &&
                          ara_fused_supported(maxrows, bs, window);
   int capall = 0;
   for (int s = 0; s < T; ++s) capall = std::max(capall, S.cap[s]);
@@ -185,7 +187,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     std::vector<long long> woff(T);
     for (int s = 0; s < T; ++s) {
       woff[s] = wtot;
-      wtot += (long long)((fo.Ad.empty() || !fo.Ad[s] ? fo.kA[s] + fo.K : 0) + 1) * bs;
+      wtot += (long long)((fo.Ad.empty() || !fo.Ad[s] ? fo.kA[s] + fo.K : 0) + 2) * bs;
     }
     double* Wb = C.buf<double>("fusedW", (size_t)wtot);
     double* rc = C.buf<double>("fusedRC", (size_t)T * capmax);

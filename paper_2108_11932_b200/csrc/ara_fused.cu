@@ -23,17 +23,17 @@ namespace tlrg {
 
 namespace {
 
-constexpr int FT = 256;         // threads per CTA
+constexpr int FT = 512;         // threads per CTA (one thread per tile row)
 constexpr int FW = FT / 32;     // warps
-constexpr int RED = 2048;       // doubles of split-k partial buffer (8 warps x 64 x NT<=4)
+constexpr int MAXROWS = 512;
+constexpr int PART_UNITS = 16;  // split-k partial tiles kept in shared memory
 
 struct FSmem {
   double* Y;      // ldy x bs
   double* R;      // bs x bs
   double* Rp;     // bs x bs
   double* Rt;     // bs x bs
-  double* part;   // RED
-  double* stg;    // 2 x stg_half (GEMM staging)
+  double* part;   // PART_UNITS x 64 x NT
   double* cbuf;   // bs (coefficients)
   double* wred;   // FW
   double* tiny;   // bs
@@ -57,188 +57,148 @@ __device__ __forceinline__ double cta_sum(double v, double* wred) {
   return s;
 }
 
-// ---- CTA GEMMs with cp.async-staged operands (double-buffered) -----------
-// Global operands are streamed through shared memory in chunks so that each
-// thread keeps many loads in flight; the FP64 tensor pipe (DMMA.8x8x4) reads
-// bank-conflict-free fragments (row strides = 4 mod 16 doubles).
-constexpr int KC = 32;           // TN: k-chunk (reduction rows per stage)
-constexpr int MB = 64;           // TN: output rows per block (8 warps x 8)
-constexpr int LAT = KC + 4;      // TN: smem row stride
-constexpr int KN = 8;            // NN: A columns per stage
-constexpr int MAXROWS = 512;     // NN: output rows (8 m-tiles per warp)
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
 
-__device__ __forceinline__ int nn_ld(int rows) { return ((rows + 15) / 16) * 16 + 4; }
+// ---- CTA GEMMs on the FP64 tensor pipe with direct 16-byte fragment loads --
+// Every lane owns a PAIR of consecutive reduction indices per 8-k block and
+// feeds them to two DMMA.8x8x4 (the k order inside a block is immaterial as
+// long as both operands agree), so each fragment load is one 128-bit access.
+// Operands live in L2 (streamed once per round) or shared memory.
 
-// out(m, n, v): v = sgn(m) * sum_{k<Kd} acol(m)[k] * B(k, n),  m < M, n < NT*8.
-// B is global (staged, ld ldb) or, with B_SMEM, read directly from shared memory.
-template <int NT, bool B_SMEM, class ACol, class Sgn, class Out>
-__device__ void gemm_tn(int M, int Kd, ACol acol, const double* B, long long ldb, Sgn sgn,
-                        Out out, double* stg, long long stg_half, double* part) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  const int nmb = (M + MB - 1) / MB, nkc = (Kd + KC - 1) / KC;
-  const int total = nmb * nkc;
-  if (total == 0) return;
-  auto issue = [&](int c) {
-    const int mb = c / nkc, kc = c % nkc;
-    double* sA = stg + (c & 1) * stg_half;
-    double* sB = sA + MB * LAT;
-    for (int e = tid; e < MB * KC; e += FT) {
-      const int mm = e / KC, kk = e % KC;
-      const int m = mb * MB + mm, k = kc * KC + kk;
-      const bool v = m < M && k < Kd;
-      cp_async8(&sA[mm * LAT + kk], v ? acol(m) + k : acol(0), v);
-    }
-    if (!B_SMEM)
-      for (int e = tid; e < NT * 8 * KC; e += FT) {
-        const int n = e / KC, kk = e % KC, k = kc * KC + kk;
-        const bool v = k < Kd;
-        cp_async8(&sB[n * LAT + kk], v ? B + k + (long long)n * ldb : B, v);
-      }
-    cp_async_commit();
-  };
-  double acc[NT][2];
+// out(m, n, v): v = sgn(m) * sum_{k<Kd} acol(m)[k] * bcol(n)[k],  m < M, n < NT*8.
+// Kd even; acol/bcol columns 16-byte aligned.  Split-k over warps when M is
+// small, partial tiles reduced in a fixed order (deterministic).
+template <int NT, class ACol, class BCol, class Sgn, class Out>
+__device__ void tn16(int M, int Kd, ACol acol, BCol bcol, Sgn sgn, Out out, double* part) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int mtiles = (M + 7) / 8;
+  if (mtiles == 0 || Kd <= 0) return;
+  int ks = FW / mtiles;
+  if (ks < 1) ks = 1;
+  if (ks * mtiles > PART_UNITS) ks = PART_UNITS / mtiles > 0 ? PART_UNITS / mtiles : 1;
+  const int k8 = (Kd + 7) / 8;
+  const int per = (k8 + ks - 1) / ks;
+  const int units = mtiles * ks;
+  for (int u = warp; u < units; u += FW) {
+    const int mt = u % mtiles, kc = u / mtiles;
+    const int m = mt * 8 + g;
+    const bool mv = m < M;
+    const double* ap = mv ? acol(m) : nullptr;
+    const double* bp[NT];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
-  issue(0);
-  for (int c = 0; c < total; ++c) {
-    if (c + 1 < total) {
-      issue(c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int mb = c / nkc, kc = c % nkc;
-    const int mtb = min(8, (M - mb * MB + 7) / 8);
-#ifdef TLRG_FUSED_NOSPLIT
-    const int ksp = 1;
-    const int mt = warp, kp = warp < mtb ? 0 : 1;
-#else
-    const int ksp = 8 / mtb;
-    const int mt = warp % mtb, kp = warp / mtb;
-#endif
-    const double* sA = stg + (c & 1) * stg_half;
-    const double* sB = sA + MB * LAT;
-    if (kp < ksp) {
-      for (int st = kp; st < KC / 4; st += ksp) {
-        const double a = sA[(mt * 8 + g) * LAT + st * 4 + t];
-        double b[NT];
-        if (B_SMEM) {
-          const int k = kc * KC + st * 4 + t;
+    for (int j = 0; j < NT; ++j) bp[j] = bcol(j * 8 + g);
+    const int b_lo = kc * per, b_hi = min(k8, b_lo + per);
+    double acc[NT][2];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) b[j] = k < Kd ? B[k + (long long)(j * 8 + g) * ldb] : 0.0;
-        } else {
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 2
+    for (int kb = b_lo; kb < b_hi; ++kb) {
+      const int kk = kb * 8 + 2 * t;
+      const bool kv = kk < Kd;
+      const double2 a = (mv && kv) ? ld2(ap + kk) : make_double2(0.0, 0.0);
+      double2 b[NT];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) b[j] = sB[(j * 8 + g) * LAT + st * 4 + t];
-        }
+      for (int j = 0; j < NT; ++j) b[j] = kv ? ld2(bp[j] + kk) : make_double2(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[j][0], acc[j][1], a, b[j]);
+      for (int j = 0; j < NT; ++j) {
+        dmma_8x8x4(acc[j][0], acc[j][1], a.x, b[j].x);
+        dmma_8x8x4(acc[j][0], acc[j][1], a.y, b[j].y);
       }
     }
-    __syncthreads();
-    if (kc == nkc - 1) {
-      // block epilogue: reduce the split-k partials in a fixed order
-      if (ksp > 1) {
-        double* P = part + warp * 64 * NT;
+    if (ks == 1) {
+      if (mv) {
+        const double sg = sgn(m);
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-          P[g * 8 * NT + j * 8 + 2 * t] = acc[j][0];
-          P[g * 8 * NT + j * 8 + 2 * t + 1] = acc[j][1];
-        }
-        __syncthreads();
-        for (int e = tid; e < mtb * 64 * NT; e += FT) {
-          const int mt2 = e / (64 * NT), r = e % (64 * NT);
-          const int gi = r / (8 * NT), n = r % (8 * NT);
-          const int m = mb * MB + mt2 * 8 + gi;
-          if (m >= M) continue;
-          double sum = 0.0;
-          for (int k2 = 0; k2 < ksp; ++k2) sum += part[(k2 * mtb + mt2) * 64 * NT + r];
-          out(m, n, sgn(m) * sum);
-        }
-        __syncthreads();
-      } else if (kp < ksp) {  // idle warps (mtb does not divide 8) hold zeros
-        const int m = mb * MB + mt * 8 + g;
-        if (m < M) {
-          const double sg = sgn(m);
-#pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            out(m, j * 8 + 2 * t, sg * acc[j][0]);
-            out(m, j * 8 + 2 * t + 1, sg * acc[j][1]);
-          }
+          out(m, j * 8 + 2 * t, sg * acc[j][0]);
+          out(m, j * 8 + 2 * t + 1, sg * acc[j][1]);
         }
       }
+    } else {
+      double* P = part + (long long)u * 64 * NT;
 #pragma unroll
-      for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+      for (int j = 0; j < NT; ++j) {
+        P[g * 8 * NT + j * 8 + 2 * t] = acc[j][0];
+        P[g * 8 * NT + j * 8 + 2 * t + 1] = acc[j][1];
+      }
+    }
+  }
+  if (ks > 1) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < mtiles * 64 * NT; e += FT) {
+      const int mt = e / (64 * NT), r = e % (64 * NT);
+      const int m = mt * 8 + r / (8 * NT), n = r % (8 * NT);
+      if (m >= M) continue;
+      double sum = 0.0;
+      for (int kc = 0; kc < ks; ++kc) sum += part[((long long)kc * mtiles + mt) * 64 * NT + r];
+      out(m, n, sgn(m) * sum);
     }
   }
   __syncthreads();
 }
 
-// epi(m, n, v): v = sum_{k<Kd} acol(k)[m] * B[k + n*ldb],  m < rows (<= 512), n < NT*8.
+// epi(r, c, v): v = sum_{k<Kd} acol(k)[r] * B[k + c*ldb],  r < rows (even, <= 512),
+// c < NT*8.  Computed as (B^T A^T): the small operand B is the DMMA "A" side and
+// every lane loads two consecutive tile rows (even/odd 8-row DMMA tiles) with
+// one 128-bit access (ldb even, 16-byte aligned columns).
 template <int NT, class ACol, class Epi>
-__device__ void gemm_nn(int rows, int Kd, ACol acol, const double* B, long long ldb, Epi epi,
-                        double* stg, long long stg_half) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  const int lda = nn_ld(rows);
-  const int nch = (Kd + KN - 1) / KN;
-  if (nch == 0) return;
-  auto issue = [&](int c) {
-    double* sA = stg + (c & 1) * stg_half;
-    double* sB = sA + KN * lda;
-    for (int e = tid; e < KN * rows; e += FT) {
-      const int kk = e / rows, r = e % rows, k = c * KN + kk;
-      const bool v = k < Kd;
-      cp_async8(&sA[kk * lda + r], v ? acol(k) + r : B, v);
+__device__ void nn16(int rows, int Kd, ACol acol, const double* B, int ldb, Epi epi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  constexpr int GPW = MAXROWS / 16 / FW;  // 16-row groups per warp
+  const int ngr = (rows + 15) / 16;
+  double acc[GPW][NT][2][2];
+#pragma unroll
+  for (int i = 0; i < GPW; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+  const int k8 = (Kd + 7) / 8;
+#pragma unroll 2
+  for (int kb = 0; kb < k8; ++kb) {
+    const int kk = kb * 8 + 2 * t;
+    double2 aw[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const double* bj = B + kk + (long long)(j * 8 + g) * ldb;
+      aw[j] = kk + 1 < Kd ? ld2(bj) : make_double2(kk < Kd ? bj[0] : 0.0, 0.0);
     }
-    for (int e = tid; e < NT * 8 * KN; e += FT) {
-      const int n = e / KN, kk = e % KN, k = c * KN + kk;
-      const bool v = k < Kd;
-      cp_async8(&sB[n * (KN + 4) + kk], v ? B + k + (long long)n * ldb : B, v);
-    }
-    cp_async_commit();
-  };
-  constexpr int MTW = MAXROWS / 64;
-  double acc[MTW][NT][2];
+    const double* c0 = kk < Kd ? acol(kk) : nullptr;
+    const double* c1 = kk + 1 < Kd ? acol(kk + 1) : nullptr;
 #pragma unroll
-  for (int i = 0; i < MTW; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  issue(0);
-  for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) {
-      issue(c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* sA = stg + (c & 1) * stg_half;
-    const double* sB = sA + KN * lda;
-#pragma unroll
-    for (int st = 0; st < KN / 4; ++st) {
-      double b[NT];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = sB[(j * 8 + g) * (KN + 4) + st * 4 + t];
-#pragma unroll
-      for (int i = 0; i < MTW; ++i) {
-        const int m = (warp + 8 * i) * 8 + g;
-        if ((warp + 8 * i) * 8 < rows) {
-          const double a = sA[(st * 4 + t) * lda + m];
-#pragma unroll
-          for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a, b[j]);
-        }
+    for (int i = 0; i < GPW; ++i) {
+      const int gr = warp + FW * i;
+      const int r = gr * 16 + 2 * g;
+      double2 b0 = make_double2(0.0, 0.0), b1 = make_double2(0.0, 0.0);
+      if (gr < ngr && r < rows) {
+        if (c0) b0 = ld2(c0 + r);
+        if (c1) b1 = ld2(c1 + r);
       }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < MTW; ++i) {
-    const int m = (warp + 8 * i) * 8 + g;
-    if (m < rows) {
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        epi(m, j * 8 + 2 * t, acc[i][j][0]);
-        epi(m, j * 8 + 2 * t + 1, acc[i][j][1]);
+        dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], aw[j].x, b0.x);
+        dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], aw[j].x, b0.y);
+        dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], aw[j].y, b1.x);
+        dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], aw[j].y, b1.y);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < GPW; ++i) {
+    const int gr = warp + FW * i;
+    if (gr >= ngr) continue;
+    const int r0 = gr * 16 + 4 * t;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int c = j * 8 + g;
+      // even tile: rows r0, r0 + 2; odd tile: rows r0 + 1, r0 + 3
+      if (r0 < rows) {
+        epi(r0, c, acc[i][j][0][0]);
+        epi(r0 + 1, c, acc[i][j][1][0]);
+      }
+      if (r0 + 2 < rows) {
+        epi(r0 + 2, c, acc[i][j][0][1]);
+        epi(r0 + 3, c, acc[i][j][1][1]);
       }
     }
   }
@@ -363,7 +323,7 @@ __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(FT) ara_fused_kernel(FusedArgs A) {
+__global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
   extern __shared__ __align__(16) double fsm[];
   const int s = blockIdx.x;
   const FusedSlot& sl = A.slots[s];
@@ -378,8 +338,7 @@ __global__ void __launch_bounds__(FT) ara_fused_kernel(FusedArgs A) {
     S.R = p; p += bs * bs;
     S.Rp = p; p += bs * bs;
     S.Rt = p; p += bs * bs;
-    S.part = p; p += RED;
-    S.stg = p; p += 2 * A.stg_half;
+    S.part = p; p += PART_UNITS * 64 * NT;
     S.cbuf = p; p += bs;
     S.wred = p; p += FW;
     S.tiny = p; p += bs;
@@ -406,9 +365,11 @@ __global__ void __launch_bounds__(FT) ara_fused_kernel(FusedArgs A) {
   TileCtx T{&sl, A.G, s, rows, cols, bs, ldy, 0, &s_cur};
   const double* gb = A.G.buf + (long long)s * A.G.cap;
   const int kA = sl.kA, K = A.K, KW = kA + K;
+  const int ldw = (KW + 1) & ~1;
 
   while (!s_done && s_rounds < A.max_rounds) {
     // ---- draw: make sure Omega and every possible replacement are available
+    const double* Om;
     {
       const long long need = (long long)cols * bs + 2LL * bs * rows;
       if (s_av - s_cur < need) {
@@ -420,29 +381,36 @@ __global__ void __launch_bounds__(FT) ara_fused_kernel(FusedArgs A) {
         if (threadIdx.x == 0) s_av = A.G.avail[s];
         __syncthreads();
       }
-      ring_copy(gb, A.G.cap, s_cur, (long long)cols * bs, sl.Om, FT);
+      const long long cur = s_cur, n = (long long)cols * bs;
+      const long long start = cur % A.G.cap;
+      if (start + n <= A.G.cap) {
+        Om = gb + start;  // contiguous in the ring: read in place
+      } else {
+        ring_copy(gb, A.G.cap, cur, n, sl.Om, FT);
+        Om = sl.Om;
+      }
       __syncthreads();
-      if (threadIdx.x == 0) s_cur += (long long)cols * bs;
+      if (threadIdx.x == 0) s_cur = cur + n;
     }
     // ---- sample -------------------------------------------------------------
     if (sl.Ad) {
       // dense operator: Y = A_tile Omega
-      gemm_nn<NT>(
-          rows, cols, [&](int k) { return sl.Ad + (long long)k * sl.ldad; }, sl.Om, cols,
-          [&](int m, int n, double v) { S.Y[m + n * ldy] = v; }, S.stg, A.stg_half);
+      nn16<NT>(
+          rows, cols, [&](int k) { return sl.Ad + (long long)k * sl.ldad; }, Om, cols,
+          [&](int m, int n, double v) { S.Y[m + n * ldy] = v; });
     } else {
-      // W = [V^A | -U_k,:]^T Omega
-      gemm_tn<NT, false>(
+      // W = [V^A | -U_k,:]^T Omega   (KW x bs, ld ldw)
+      tn16<NT>(
           KW, cols,
           [&](int m) { return m < kA ? sl.VA + (long long)m * cols : A.Ucat + (long long)(m - kA) * cols; },
-          sl.Om, cols, [&](int m) { return m < kA ? 1.0 : -1.0; },
-          [&](int m, int n, double v) { sl.W[m + (long long)n * KW] = v; }, S.stg, A.stg_half,
-          S.part);
+          [&](int n) { return Om + (long long)n * cols; },
+          [&](int m) { return m < kA ? 1.0 : -1.0; },
+          [&](int m, int n, double v) { sl.W[m + (long long)n * ldw] = v; }, S.part);
       // Y = [U^A | H] W
-      gemm_nn<NT>(
+      nn16<NT>(
           rows, KW,
           [&](int k) { return k < kA ? sl.UA + (long long)k * rows : sl.H + (long long)(k - kA) * rows; },
-          sl.W, KW, [&](int m, int n, double v) { S.Y[m + n * ldy] = v; }, S.stg, A.stg_half);
+          sl.W, ldw, [&](int m, int n, double v) { S.Y[m + n * ldy] = v; });
     }
     // ---- orthog (dense_kernels.cpp:379-420) ------------------------------------
     {
@@ -461,16 +429,16 @@ __global__ void __launch_bounds__(FT) ara_fused_kernel(FusedArgs A) {
     T.q = s_q;
     for (int sweep = 0; sweep < 2; ++sweep) {
       if (T.q > 0) {
-        const int q = T.q;
+        const int q = T.q, ldc = (q + 1) & ~1;
         // C = Q^T Y
-        gemm_tn<NT, true>(
-            q, rows, [&](int m) { return sl.Q + (long long)m * rows; }, S.Y, ldy,
-            [](int) { return 1.0; }, [&](int m, int n, double v) { sl.Cq[m + (long long)n * q] = v; },
-            S.stg, A.stg_half, S.part);
+        tn16<NT>(
+            q, rows, [&](int m) { return sl.Q + (long long)m * rows; },
+            [&](int n) { return (const double*)(S.Y + n * ldy); }, [](int) { return 1.0; },
+            [&](int m, int n, double v) { sl.Cq[m + (long long)n * ldc] = v; }, S.part);
         // Y -= Q C
-        gemm_nn<NT>(
-            rows, q, [&](int k) { return sl.Q + (long long)k * rows; }, sl.Cq, q,
-            [&](int m, int n, double v) { S.Y[m + n * ldy] -= v; }, S.stg, A.stg_half);
+        nn16<NT>(
+            rows, q, [&](int k) { return sl.Q + (long long)k * rows; }, sl.Cq, ldc,
+            [&](int m, int n, double v) { S.Y[m + n * ldy] -= v; });
       }
       panel_sweep<NT>(T, S, sweep, s_tau);
     }
@@ -528,12 +496,6 @@ __global__ void __launch_bounds__(FT) ara_fused_kernel(FusedArgs A) {
   }
 }
 
-long long fused_stg_half(int maxrows, int bs) {
-  long long tn = (long long)(MB + bs) * LAT;
-  long long nn = (long long)KN * (((maxrows + 15) / 16) * 16 + 4) + (long long)bs * (KN + 4);
-  long long h = tn > nn ? tn : nn;
-  return (h + 1) & ~1LL;
-}
 size_t fused_smem_bytes(int maxrows, int bs, int window, int* ldy, long long* ysz) {
   int l = ((maxrows + 15) / 16) * 16 + 4;
   long long y = (long long)l * bs;
@@ -542,14 +504,15 @@ size_t fused_smem_bytes(int maxrows, int bs, int window, int* ldy, long long* ys
   y = (y + 1) & ~1LL;
   *ldy = l;
   *ysz = y;
-  long long d = y + 3LL * bs * bs + RED + 2 * fused_stg_half(maxrows, bs) + bs + FW + 3LL * bs + window + bs /*keep ints*/ + bs;
+  long long d = y + 3LL * bs * bs + (long long)PART_UNITS * 64 * (bs / 8) + bs + FW + 3LL * bs +
+                window + bs /*keep ints*/ + bs;
   return (size_t)d * 8 + 64;
 }
 
 }  // namespace
 
 bool ara_fused_supported(int maxrows, int bs, int window) {
-  if (maxrows > MAXROWS) return false;
+  if (maxrows > MAXROWS) return false;  // callers also need even rows / cols
   if (bs != 8 && bs != 16 && bs != 24 && bs != 32) return false;
   int ldy;
   long long ysz;
@@ -569,7 +532,7 @@ void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st) {
   long long ysz;
   size_t bytes = fused_smem_bytes(maxrows, bs, args.window, &args.ldy, &ysz);
   args.ysz = ysz;
-  args.stg_half = fused_stg_half(maxrows, bs);
+  args.stg_half = 0;
   switch (bs) {
 #define TLRG_FUSED_CASE(NT)                                                                 \
   case NT * 8: {                                                                            \
