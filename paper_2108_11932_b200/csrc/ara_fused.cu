@@ -35,6 +35,7 @@ struct FSmem {
   double* Rt;     // bs x bs
   double* part;   // PART_UNITS x 64 x NT
   double* cbuf;   // bs (coefficients)
+  double* wpart;  // FW x 32 per-warp partial coefficient vectors
   double* wred;   // FW
   double* tiny;   // bs
   double* cn;     // bs
@@ -205,35 +206,6 @@ __device__ void nn16(int rows, int Kd, ACol acol, const double* B, int ldb, Epi 
   __syncthreads();
 }
 
-// one classical pass of column j against the panel columns p < j; the
-// coefficients land in S.cbuf (and are added to Rp(:, j) when rp != null)
-__device__ void cgs_pass(double* Y, int ldy, int rows, int j, FSmem& S, double* rp) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double* yj = Y + (long long)j * ldy;
-  for (int p = warp; p < j; p += FW) {
-    const double* yp = Y + (long long)p * ldy;
-    double s = 0.0;
-    for (int r = lane; r < rows; r += 32) s += yp[r] * yj[r];
-    s = warp_sum(s);
-    if (lane == 0) S.cbuf[p] = s;
-  }
-  __syncthreads();
-  if (rp && threadIdx.x < j) rp[threadIdx.x] += S.cbuf[threadIdx.x];
-  double* yw = Y + (long long)j * ldy;
-  for (int r = threadIdx.x; r < rows; r += FT) {
-    double acc = 0.0;
-    for (int p = 0; p < j; ++p) acc += S.cbuf[p] * Y[(long long)p * ldy + r];
-    yw[r] -= acc;
-  }
-  __syncthreads();
-}
-
-__device__ double col_norm(const double* y, int rows, FSmem& S) {
-  double s = 0.0;
-  for (int r = threadIdx.x; r < rows; r += FT) s += y[r] * y[r];
-  return sqrt(cta_sum(s, S.wred));
-}
-
 struct TileCtx {
   const FusedSlot* sl;
   GaussStreams G;
@@ -241,80 +213,178 @@ struct TileCtx {
   long long* cur;  // smem cursor (absolute stream position)
 };
 
-// panel MGS2 of one sweep (dense_kernels.cpp:331-375) on the smem panel; Rp is
-// accumulated, deficient columns are replaced from the tile's stream and
-// projected against Q and the earlier panel columns.
+// Reduce-scatter of N (16 or 32) values over a warp: afterwards every lane
+// holds the full warp sum of index (lane >> 1) (N = 16) or lane (N = 32).
+template <int N>
+__device__ __forceinline__ double warp_reduce_scatter(double (&v)[N]) {
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  double w[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i] = v[i];
+#pragma unroll
+  for (int half = N / 2, bit = 16; half >= 1; half >>= 1, bit >>= 1) {
+    const bool hi = (lane & bit) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = hi ? w[i] : w[i + half];
+      const double keep = hi ? w[i + half] : w[i];
+      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+    }
+    base += hi ? half : 0;
+  }
+  double r = w[0];
+  if (N == 16) r += __shfl_xor_sync(0xffffffffu, r, 1);
+  return r;
+}
+
+// one classical pass of column j of the register-resident panel against the
+// columns p < j (each thread owns one tile row); coefficients land in S.cbuf
+// and are added to Rp(:, j) when add_r.  Two CTA barriers.
+template <int BS, int J>
+__device__ __forceinline__ void cgs_pass_reg(double (&y)[BS], FSmem& S, double* rpj) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int N = J <= 16 ? 16 : 32;
+  double part[N];
+#pragma unroll
+  for (int p = 0; p < N; ++p) part[p] = p < J ? y[p] * y[J] : 0.0;
+  const double red = warp_reduce_scatter<N>(part);
+  if (N == 32) {
+    S.wpart[warp * 32 + lane] = red;
+  } else if ((lane & 1) == 0) {
+    S.wpart[warp * 32 + (lane >> 1)] = red;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < J) {
+    double c = 0.0;
+#pragma unroll
+    for (int w = 0; w < FW; ++w) c += S.wpart[w * 32 + threadIdx.x];
+    S.cbuf[threadIdx.x] = c;
+    if (rpj) rpj[threadIdx.x] += c;
+  }
+  __syncthreads();
+  double acc = 0.0;
+#pragma unroll
+  for (int p = 0; p < J; ++p) acc += S.cbuf[p] * y[p];
+  y[J] -= acc;
+}
+
+__device__ __forceinline__ double cta_norm(double v, FSmem& S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v * v);
+  if (lane == 0) S.wred[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < FW; ++w) s += S.wred[w];
+  return sqrt(s);
+}
+
+// panel MGS2 of one sweep (dense_kernels.cpp:331-375) with the panel held in
+// registers (row r of the tile in thread r); Rp is accumulated, deficient
+// columns are replaced from the tile's stream and projected against Q and the
+// earlier panel columns.
+template <int BS, int J>
+__device__ __forceinline__ void mgs_column(TileCtx& T, FSmem& S, double (&y)[BS], double tau) {
+  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+  const bool rv = r < T.rows;
+  double* rpj = S.Rp + J * BS;
+  if (J > 0) {
+    cgs_pass_reg<BS, J>(y, S, rpj);
+    cgs_pass_reg<BS, J>(y, S, rpj);
+  }
+  double nj = cta_norm(y[J], S);
+  if (!(nj >= tau)) {
+    if (threadIdx.x == 0 && !S.defi[J]) {
+      S.defi[J] = 1;
+      S.tiny[J] = isfinite(nj) ? nj : 0.0;
+    }
+    // fresh direction from the tile's own stream: y <- g - Q (Q^T g)
+    const long long c0 = *T.cur;
+    __syncthreads();
+    if (threadIdx.x == 0) *T.cur = c0 + T.rows;
+    const double* gb = T.G.buf + (long long)T.s * T.G.cap;
+    y[J] = rv ? gb[(c0 + r) % T.G.cap] : 0.0;
+    const int q = T.q;
+    if (q > 0) {
+      const FusedSlot& sl = *T.sl;
+      double* yj = S.Y + (long long)J * T.ldy;
+      if (rv) yj[r] = y[J];
+      __syncthreads();
+      for (int tq = warp; tq < q; tq += FW) {
+        const double* qt = sl.Q + (long long)tq * T.rows;
+        double s = 0.0;
+        for (int i = lane; i < T.rows; i += 32) s += qt[i] * yj[i];
+        s = warp_sum(s);
+        if (lane == 0) sl.repC[tq] = s;
+      }
+      __syncthreads();
+      if (rv) {
+        double s = 0.0;
+        for (int tq = 0; tq < q; ++tq) s += sl.Q[(long long)tq * T.rows + r] * sl.repC[tq];
+        y[J] -= s;
+      }
+    }
+    if (J > 0) {
+      cgs_pass_reg<BS, J>(y, S, nullptr);
+      cgs_pass_reg<BS, J>(y, S, nullptr);
+    }
+    __syncthreads();  // wred reuse
+    nj = cta_norm(y[J], S);
+    if (nj == 0.0) {
+      y[J] = (r == J % T.rows) ? 1.0 : 0.0;
+      nj = 1.0;
+    }
+    if (threadIdx.x == 0) rpj[J] = 0.0;
+  } else {
+    if (threadIdx.x == 0) rpj[J] = nj;
+  }
+  y[J] *= 1.0 / nj;
+}
+
+template <int BS, int J>
+struct MgsUnroll {
+  __device__ __forceinline__ static void run(TileCtx& T, FSmem& S, double (&y)[BS], double tau) {
+    mgs_column<BS, J>(T, S, y, tau);
+    MgsUnroll<BS, J + 1>::run(T, S, y, tau);
+  }
+};
+template <int BS>
+struct MgsUnroll<BS, BS> {
+  __device__ __forceinline__ static void run(TileCtx&, FSmem&, double (&)[BS], double) {}
+};
+
 template <int NT>
 __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
-  const int rows = T.rows, w = T.bs, ldy = T.ldy, q = T.q;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* Y = S.Y;
-  for (int e = threadIdx.x; e < w * w; e += FT) S.Rp[e] = 0.0;
+  constexpr int BS = NT * 8;
+  const int r = threadIdx.x;
+  const bool rv = r < T.rows;
+  for (int e = threadIdx.x; e < BS * BS; e += FT) S.Rp[e] = 0.0;
   if (sweep == 0)
-    for (int j = threadIdx.x; j < w; j += FT) {
+    for (int j = threadIdx.x; j < BS; j += FT) {
       S.defi[j] = 0;
       S.tiny[j] = 0.0;
     }
+  double y[BS];
+#pragma unroll
+  for (int c = 0; c < BS; ++c) y[c] = rv ? S.Y[r + c * T.ldy] : 0.0;
   __syncthreads();
-  const FusedSlot& sl = *T.sl;
-  const double* gb = T.G.buf + (long long)T.s * T.G.cap;
-  for (int j = 0; j < w; ++j) {
-    double* yj = Y + (long long)j * ldy;
-    if (j > 0)
-      for (int pass = 0; pass < 2; ++pass) cgs_pass(Y, ldy, rows, j, S, S.Rp + (long long)j * w);
-    double nj = col_norm(yj, rows, S);
-    if (!(nj >= tau)) {
-      if (threadIdx.x == 0 && !S.defi[j]) {
-        S.defi[j] = 1;
-        S.tiny[j] = isfinite(nj) ? nj : 0.0;
-      }
-      // fresh direction from the tile's own stream: y <- g - Q (Q^T g)
-      const long long c0 = *T.cur;
-      __syncthreads();
-      if (threadIdx.x == 0) *T.cur = c0 + rows;
-      ring_copy(gb, T.G.cap, c0, rows, yj, FT);
-      __syncthreads();
-      if (q > 0) {
-        double* rc = sl.repC;
-        for (int tq = warp; tq < q; tq += FW) {
-          const double* qt = sl.Q + (long long)tq * rows;
-          double s = 0.0;
-          for (int r = lane; r < rows; r += 32) s += qt[r] * yj[r];
-          s = warp_sum(s);
-          if (lane == 0) rc[tq] = s;
-        }
-        __syncthreads();
-        for (int r = threadIdx.x; r < rows; r += FT) {
-          double s = 0.0;
-          for (int tq = 0; tq < q; ++tq) s += sl.Q[(long long)tq * rows + r] * rc[tq];
-          yj[r] -= s;
-        }
-        __syncthreads();
-      }
-      if (j > 0)
-        for (int pass = 0; pass < 2; ++pass) cgs_pass(Y, ldy, rows, j, S, nullptr);
-      nj = col_norm(yj, rows, S);
-      if (nj == 0.0) {
-        if (threadIdx.x == 0) yj[j % rows] = 1.0;
-        nj = 1.0;
-      }
-      if (threadIdx.x == 0) S.Rp[j + (long long)j * w] = 0.0;
-    } else {
-      if (threadIdx.x == 0) S.Rp[j + (long long)j * w] = nj;
-    }
-    const double inv = 1.0 / nj;
-    for (int r = threadIdx.x; r < rows; r += FT) yj[r] *= inv;
-    __syncthreads();
+  MgsUnroll<BS, 0>::run(T, S, y, tau);
+  if (rv) {
+#pragma unroll
+    for (int c = 0; c < BS; ++c) S.Y[r + c * T.ldy] = y[c];
   }
+  __syncthreads();
   // R <- Rp R   (R = I before the first sweep)
+  const int w = BS;
   if (sweep == 0) {
     for (int e = threadIdx.x; e < w * w; e += FT) S.R[e] = S.Rp[e];
   } else {
     for (int e = threadIdx.x; e < w * w; e += FT) {
       const int p = e % w, jj = e / w;
-      double s = 0.0;
-      for (int tt = p; tt <= jj; ++tt) s += S.Rp[p + tt * w] * S.R[tt + jj * w];
-      S.Rt[e] = p <= jj ? s : 0.0;
+      double sum = 0.0;
+      for (int tt = p; tt <= jj; ++tt) sum += S.Rp[p + tt * w] * S.R[tt + jj * w];
+      S.Rt[e] = p <= jj ? sum : 0.0;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < w * w; e += FT) S.R[e] = S.Rt[e];
@@ -340,6 +410,7 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
     S.Rt = p; p += bs * bs;
     S.part = p; p += PART_UNITS * 64 * NT;
     S.cbuf = p; p += bs;
+    S.wpart = p; p += FW * 32;
     S.wred = p; p += FW;
     S.tiny = p; p += bs;
     S.cn = p; p += bs;
@@ -415,10 +486,11 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
     // ---- orthog (dense_kernels.cpp:379-420) ------------------------------------
     {
       double f = 0.0;
-      for (int e = threadIdx.x; e < rows * bs; e += FT) {
-        const double y = S.Y[(e % rows) + (e / rows) * ldy];
-        f += y * y;
-      }
+      if (threadIdx.x < rows)
+        for (int c = 0; c < bs; ++c) {
+          const double y = S.Y[threadIdx.x + c * ldy];
+          f += y * y;
+        }
       f = cta_sum(f, S.wred);
       if (threadIdx.x == 0) {
         double tau = 100.0 * DBL_EPSILON * sqrt(f);
@@ -504,7 +576,8 @@ size_t fused_smem_bytes(int maxrows, int bs, int window, int* ldy, long long* ys
   y = (y + 1) & ~1LL;
   *ldy = l;
   *ysz = y;
-  long long d = y + 3LL * bs * bs + (long long)PART_UNITS * 64 * (bs / 8) + bs + FW + 3LL * bs +
+  long long d = y + 3LL * bs * bs + (long long)PART_UNITS * 64 * (bs / 8) + bs + FW * 32 + FW +
+                3LL * bs +
                 window + bs /*keep ints*/ + bs;
   return (size_t)d * 8 + 64;
 }

@@ -2,7 +2,8 @@
 import csv, subprocess, sys
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kf = sys.argv[3:] and ["--kernel-name", sys.argv[3]] or []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + kf,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 res, fname = [], ""
