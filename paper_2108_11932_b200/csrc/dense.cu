@@ -18,36 +18,43 @@ namespace cg = cooperative_groups;
 namespace tlrg {
 
 // ---------------------------------------------------------------- POTRF ---
-// Right-looking blocked Cholesky in ONE cooperative kernel over a persistent
-// grid.  Per 32-column panel p:
-//   phase 1: for each row block r >= p (CTAs in parallel) factor A_pp in shared
-//            memory (redundantly, one warp) and store L_pp (r = p) or solve
-//            L_rp = A_rp L_pp^{-T} (r > p);                       grid.sync
-//   phase 2: rank-32 update of every trailing lower tile
-//            A_rc -= L_rp L_cp^T, p < c <= r, spread over all CTAs; grid.sync
+// Right-looking blocked Cholesky in ONE cooperative kernel over a small
+// persistent grid (the diagonal path shares the GPU with the column's ARA).
+// Per 32-column panel p:
+//   phase 1: every CTA with panel rows factors A_pp redundantly in one warp's
+//            REGISTERS (lane i owns row i, column broadcasts by shuffle), then
+//            solves its rows of L_rp = A_rp L_pp^{-T} one warp per row;  grid.sync
+//   phase 2: CTA 0 stores L_pp; rank-32 update of every trailing lower 32x32
+//            tile A_rc -= L_rp L_cp^T spread over all CTAs;               grid.sync
 constexpr int PB = 32;
-constexpr int PO_T = 128;
+constexpr int PO_T = 256;
+constexpr int PO_W = PO_T / 32;
 
-__device__ __forceinline__ bool chol32_smem(double (*Lp)[PB + 1], int pw, int* fail_at) {
-  // unblocked right-looking Cholesky of the pw x pw block held by warp 0
+// unblocked Cholesky of the pw x pw block (pw <= 32) held one row per lane;
+// returns the failing column or -1.  v[j] = L(lane, j) on exit (j <= lane).
+__device__ __forceinline__ int chol32_reg(double (&v)[PB], int pw) {
   const int lane = threadIdx.x & 31;
-  for (int j = 0; j < pw; ++j) {
-    double d = Lp[j][j];
-    if (!(d > 0.0)) {
-      *fail_at = j;
-      return false;
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < PB; ++j) {
+    if (j < pw && fail < 0) {
+      const double d = __shfl_sync(0xffffffffu, v[j], j);
+      if (!(d > 0.0)) {
+        fail = j;
+      } else {
+        const double s = sqrt(d);
+        if (lane == j) v[j] = s;
+        else if (lane > j) v[j] /= s;
+        const double lij = v[j];
+#pragma unroll
+        for (int k = j + 1; k < PB; ++k) {
+          const double lkj = __shfl_sync(0xffffffffu, lij, k);
+          if (lane >= k) v[k] -= lij * lkj;
+        }
+      }
     }
-    double s = sqrt(d);
-    __syncwarp();
-    if (lane == 0) Lp[j][j] = s;
-    __syncwarp();
-    if (lane > j && lane < pw) Lp[lane][j] /= s;
-    __syncwarp();
-    if (lane > j && lane < pw)
-      for (int c = j + 1; c <= lane; ++c) Lp[lane][c] -= Lp[lane][j] * Lp[c][j];
-    __syncwarp();
   }
-  return true;
+  return fail;
 }
 
 __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int* info) {
@@ -56,60 +63,53 @@ __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int*
   __shared__ double Ar[PB][PB + 1];
   __shared__ double Lb[PB][PB + 1];
   __shared__ int s_fail;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = (n + PB - 1) / PB;
   auto bw = [&](int t) { return min(PB, n - t * PB); };
+  const int gw = gridDim.x * PO_W;  // warps in the grid
   for (int p = 0; p < nt; ++p) {
     const int p0 = p * PB, pw = bw(p);
+    const int below = n - (p0 + pw);
+    const bool mine = blockIdx.x == 0 || (int)blockIdx.x * PO_W < below;
     // ---- phase 1 -------------------------------------------------------------
-    for (int r = p + blockIdx.x; r < nt; r += gridDim.x) {
-      const int r0 = r * PB, rw = bw(r);
-      __syncthreads();
-      for (int e = tid; e < PB * PB; e += PO_T) {
-        int i = e % PB, j = e / PB;
-        Lp[i][j] = (i < pw && j < pw) ? A[(p0 + i) + (long long)(p0 + j) * n] : 0.0;
-      }
-      if (tid == 0) s_fail = -1;
-      __syncthreads();
-      if (tid < 32) {
-        int fa = -1;
-        bool ok = chol32_smem(Lp, pw, &fa);
-        if (!ok && tid == 0) s_fail = p0 + fa;
+    if (mine) {
+      if (warp == 0) {
+        double v[PB];
+#pragma unroll
+        for (int j = 0; j < PB; ++j)
+          v[j] = (lane < pw && j < pw && j <= lane) ? A[(p0 + lane) + (long long)(p0 + j) * n] : 0.0;
+        const int fa = chol32_reg(v, pw);
+#pragma unroll
+        for (int j = 0; j < PB; ++j) Lp[lane][j] = (j <= lane) ? v[j] : 0.0;
+        if (lane == 0) s_fail = fa;
       }
       __syncthreads();
       if (s_fail >= 0) {
-        if (tid == 0) atomicCAS(info, -1, s_fail);
-        continue;
-      }
-      if (r == p) {
-        // L_pp is written back after the grid sync (other CTAs of this phase
-        // still read the unfactored A_pp from global memory)
+        if (tid == 0) atomicCAS(info, -1, p0 + s_fail);
       } else {
-        for (int e = tid; e < rw * pw; e += PO_T) {
-          int i = e % rw, j = e / rw;
-          Ar[i][j] = A[(r0 + i) + (long long)(p0 + j) * n];
-        }
-        __syncthreads();
-        if (tid < rw)
-          for (int j = 0; j < pw; ++j) {
-            double s = Ar[tid][j];
-            for (int t = 0; t < j; ++t) s -= Ar[tid][t] * Lp[j][t];
-            Ar[tid][j] = s / Lp[j][j];
+        // L_rp = A_rp L_pp^{-T}: one warp per row, lane t owns x_t
+        for (int r = p0 + pw + blockIdx.x * PO_W + warp; r < n; r += gw) {
+          const double a = lane < pw ? A[r + (long long)(p0 + lane) * n] : 0.0;
+          double x = 0.0;
+#pragma unroll
+          for (int j = 0; j < PB; ++j) {
+            if (j < pw) {
+              const double part = lane < j ? x * Lp[j][lane] : 0.0;
+              const double sum = warp_sum(part);
+              const double aj = __shfl_sync(0xffffffffu, a, j);
+              const double xj = (aj - sum) / Lp[j][j];
+              if (lane == j) x = xj;
+            }
           }
-        __syncthreads();
-        for (int e = tid; e < rw * pw; e += PO_T) {
-          int i = e % rw, j = e / rw;
-          A[(r0 + i) + (long long)(p0 + j) * n] = Ar[i][j];
+          if (lane < pw) A[r + (long long)(p0 + lane) * n] = x;
         }
       }
     }
     grid.sync();
     if (*(volatile int*)info >= 0) break;
     if (blockIdx.x == 0) {
-      // CTA 0 handled r = p last with this Lp (phase 1 loop visits r = p first and
-      // every later r recomputes the same L_pp), so its copy is the factor
       for (int e = tid; e < pw * pw; e += PO_T) {
-        int i = e % pw, j = e / pw;
+        const int i = e % pw, j = e / pw;
         A[(p0 + i) + (long long)(p0 + j) * n] = i >= j ? Lp[i][j] : 0.0;
       }
     }
@@ -117,34 +117,31 @@ __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int*
     const int ntr = nt - p - 1;
     const int ntiles = ntr * (ntr + 1) / 2;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      // t -> (rr, cc) with cc <= rr in the trailing triangle
       int rr = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
       while (rr * (rr + 1) / 2 > t) --rr;
       while ((rr + 1) * (rr + 2) / 2 <= t) ++rr;
-      int cc = t - rr * (rr + 1) / 2;
+      const int cc = t - rr * (rr + 1) / 2;
       const int r = p + 1 + rr, c = p + 1 + cc;
       const int r0 = r * PB, c0 = c * PB, rw = bw(r), cw = bw(c);
       __syncthreads();
       for (int e = tid; e < PB * PB; e += PO_T) {
-        int i = e % PB, k = e / PB;
+        const int i = e % PB, k = e / PB;
         Ar[i][k] = (i < rw && k < pw) ? A[(r0 + i) + (long long)(p0 + k) * n] : 0.0;
         Lb[i][k] = (i < cw && k < pw) ? A[(c0 + i) + (long long)(p0 + k) * n] : 0.0;
       }
       __syncthreads();
-      const int ci = tid & 31, rj = tid >> 5;
-      double acc[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+      const int ci = tid & 31, rj = tid >> 5;  // 8 row groups x 32 columns
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 8
       for (int k = 0; k < PB; ++k) {
-        double bv = Lb[ci][k];
+        const double bv = Lb[ci][k];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] += Ar[rj + 4 * u][k] * bv;
+        for (int u = 0; u < 4; ++u) acc[u] += Ar[rj + 8 * u][k] * bv;
       }
       if (ci < cw)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          int i = rj + 4 * u;
+        for (int u = 0; u < 4; ++u) {
+          const int i = rj + 8 * u;
           if (i < rw) A[(r0 + i) + (long long)(c0 + ci) * n] -= acc[u];
         }
     }
@@ -153,7 +150,7 @@ __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int*
   // zero the strict upper triangle (dense_kernels.cpp:79-80)
   for (long long e = blockIdx.x * (long long)PO_T + tid; e < (long long)n * n;
        e += (long long)gridDim.x * PO_T) {
-    int i = (int)(e % n), j = (int)(e / n);
+    const int i = (int)(e % n), j = (int)(e / n);
     if (i < j) A[e] = 0.0;
   }
 }
@@ -181,9 +178,40 @@ void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st) {
   set_int_kernel<<<1, 1, 0, st>>>(info, -1);
   int nt = (n + PB - 1) / PB;
   int grid = coop_grid((const void*)potrf_coop_kernel, PO_T, std::max(nt, nt * (nt - 1) / 2));
+  if (grid > 48) grid = 48;
   void* args[] = {&A, &n, &info};
   TLRG_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel, dim3(grid), dim3(PO_T), args, 0,
                                         st));
+}
+
+// ------------------------------------------------------- TRTRI (base) -----
+// X_bb = L_bb^{-1} for a list of diagonal blocks (<= 32 x 32), one CTA per
+// block, one warp per right-hand-side column (lane i owns row i).
+__global__ void __launch_bounds__(256) trtri_base_kernel(const double* L, int n, double* X,
+                                                         const int* offs, const int* lens) {
+  __shared__ double Ls[32][33];
+  const int o = offs[blockIdx.x], len = lens[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < 32 * 32; e += 256) {
+    const int i = e % 32, k = e / 32;
+    Ls[i][k] = (i < len && k <= i) ? L[(o + i) + (long long)(o + k) * n] : 0.0;
+  }
+  __syncthreads();
+  for (int j = warp; j < len; j += 8) {
+    double x = lane == j ? 1.0 : 0.0;
+    for (int k = j; k < len; ++k) {
+      const double xk = __shfl_sync(0xffffffffu, x, k) / Ls[k][k];
+      if (lane == k) x = xk;
+      if (lane > k) x -= Ls[lane][k] * xk;
+    }
+    if (lane < len && lane >= j) X[(o + lane) + (long long)(o + j) * n] = x;
+  }
+}
+void trtri_base(const double* L, int n, double* X, const int* d_offs, const int* d_lens,
+                int nblocks, cudaStream_t st) {
+  if (nblocks <= 0) return;
+  trtri_base_kernel<<<nblocks, 256, 0, st>>>(L, n, X, d_offs, d_lens);
+  TLRG_CUDA(cudaGetLastError());
 }
 
 // ------------------------------------------------------ BUNCH-KAUFMAN -----

@@ -122,6 +122,56 @@ void identity(double* A, int n, cudaStream_t st) {
 
 void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st);
 
+// X = L^{-1} for a lower-triangular n x n tile by recursive block inversion on
+// the grouped DMMA GEMM:  inv([L11 0; L21 L22]) = [X11 0; -X22 L21 X11  X22].
+// 32x32 diagonal blocks are inverted in one launch, then every merge level
+// (pairs of blocks) is two batched GEMMs.  Off the critical path (diagonal
+// stream); replaces a TRSM against the identity.
+void trtri_device(Ctx& C, const double* L, int n, double* X) {
+  TLRG_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * n * n, C.st));
+  std::vector<int> offs, lens;
+  for (int o = 0; o < n; o += 32) {
+    offs.push_back(o);
+    lens.push_back(std::min(32, n - o));
+  }
+  trtri_base(L, n, X, C.push(offs), C.push(lens), (int)offs.size(), C.st);
+  ++C.launches;
+  double* T = C.buf<double>("trtri_T", (size_t)n * n / 2 + 64);
+  while (offs.size() > 1) {
+    std::vector<GemmProblem> p1, p2;
+    std::vector<int> no, nl;
+    size_t toff = 0;
+    for (size_t b = 0; b + 1 < offs.size(); b += 2) {
+      const int o = offs[b], l1 = lens[b], l2 = lens[b + 1];
+      GemmProblem g{};
+      // T = L21 X11   (l2 x l1)
+      g.A = L + (o + l1) + (long long)o * n; g.lda = n;
+      g.B = X + o + (long long)o * n; g.ldb = n;
+      g.C = T + toff; g.ldc = l2;
+      g.M = l2; g.N = l1; g.K = l1; g.alpha = 1.0;
+      p1.push_back(g);
+      // X21 = -X22 T
+      GemmProblem h{};
+      h.A = X + (o + l1) + (long long)(o + l1) * n; h.lda = n;
+      h.B = T + toff; h.ldb = l2;
+      h.C = X + (o + l1) + (long long)o * n; h.ldc = n;
+      h.M = l2; h.N = l1; h.K = l2; h.alpha = -1.0;
+      p2.push_back(h);
+      toff += (size_t)l1 * l2;
+      no.push_back(o);
+      nl.push_back(l1 + l2);
+    }
+    if (offs.size() % 2) {
+      no.push_back(offs.back());
+      nl.push_back(lens.back());
+    }
+    C.gemm(p1);
+    C.gemm(p2);
+    offs.swap(no);
+    lens.swap(nl);
+  }
+}
+
 bool potrf_device(Ctx& C, double* A, int n) {
   int* info = C.buf<int>("potrf_info", 1);
   potrf_impl(A, n, info, C.desc, C.st);
@@ -381,9 +431,9 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       }
     };
     auto diag_inverse = [&]() {
-      identity(Xinv, rk, C.st);
+      if (ldl) identity(Xinv, rk, C.st);
       if (!ldl) {
-        trsm_panel(diagk, rk, Xinv, rk, nullptr, nullptr, nullptr, nullptr, info + 3, C.st);
+        trtri_device(C, diagk, rk, Xinv);
         min_diag_sq(diagk, rk, piv + k, C.st);
       } else {
         size_t o = (size_t)k * b;

@@ -203,6 +203,9 @@ void sytrf_bk(double* A, int n, double* d, double* e, uint8_t* s2, int* perm, in
 void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
                 const double* d, const double* e, const uint8_t* s2, int* info,
                 cudaStream_t st);
+// X_bb = L_bb^{-1} for diagonal blocks (offset, length <= 32) of an n x n lower L
+void trtri_base(const double* L, int n, double* X, const int* d_offs, const int* d_lens,
+                int nblocks, cudaStream_t st);
 // D <- 0.5 (D + D^T)
 void symmetrize(double* D, int n, cudaStream_t st);
 // out = A - D (+ diag(corr)) (+ shift I)
