@@ -14,6 +14,7 @@
 // + one-sided Jacobi SVD of R, cut at (1 - 1/eta) eps) in batches, and the
 // final factors are written into a contiguous panel.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 
@@ -55,6 +56,18 @@ void ara_loop_cond(cudaGraphConditionalHandle h, int* active, int max_rounds, cu
   TLRG_CUDA(cudaGetLastError());
 }
 }  // namespace
+
+bool ara_fused_eligible(int cols, const std::vector<int>& rows, int bs, int window) {
+  const char* nf = std::getenv("TLRG_NO_FUSED");
+  if (nf && nf[0] == '1') return false;
+  if (cols % 2) return false;
+  int maxrows = 0;
+  for (int r : rows) {
+    if (r % 2) return false;
+    maxrows = std::max(maxrows, r);
+  }
+  return ara_fused_supported(maxrows, bs, window);
+}
 
 void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int bs, int maxrows,
                      int rounds_ahead, StreamPrep& P) {
@@ -121,10 +134,11 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   int *qcols = ints, *rounds = ints + T, *conv = ints + 2 * T, *done = ints + 3 * T,
       *rcount = ints + 4 * T, *rpos = ints + 5 * T;
   TLRG_CUDA(cudaMemsetAsync(ints, 0, sizeof(int) * T * 6, C.st));
+  const bool use_fused = op.fused.on && ara_fused_eligible(cols, S.rows, bs, window);
   // per-tile gaussian streams (exact tlr::Rng sequences), consumed by cursor
   GaussStreams G;
   std::vector<long long> h_av(T, 0), h_cur(T, 0);
-  if (pre && pre->T == T && pre->seeds == S.seeds &&
+  if (!use_fused && pre && pre->T == T && pre->seeds == S.seeds &&
       pre->G.cap >= 2LL * cols * bs + 4LL * bs * maxrows) {
     G = pre->G;
     TLRG_CUDA(cudaStreamWaitEvent(C.st, pre->ev, 0));
@@ -169,11 +183,6 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     TLRG_CUDA(cudaMemcpyAsync(d_rows, S.rows.data(), sizeof(int) * T, cudaMemcpyHostToDevice,
                               C.st));
   }
-  const char* nf = std::getenv("TLRG_NO_FUSED");
-  bool even = (cols % 2) == 0;
-  for (int s = 0; s < T; ++s) even = even && (S.rows[s] % 2) == 0;
-  const bool use_fused = op.fused.on && !(nf && nf[0] == '1') && even &&
-                         ara_fused_supported(maxrows, bs, window);
   int capall = 0;
   for (int s = 0; s < T; ++s) capall = std::max(capall, S.cap[s]);
   const int max_rounds = 4 * capall + 8;  // a tile gains >= 1 column per round or converges
@@ -223,8 +232,35 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     fa.qcols = qcols;
     fa.rounds = rounds;
     fa.conv = conv;
+    const char* fp = std::getenv("TLRG_FUSED_PROF");
+    long long* dprof = nullptr;
+    if (fp && fp[0] == '1') {
+      dprof = C.buf<long long>("fused_prof", (size_t)T * 8);
+      fa.prof = dprof;
+    }
     ara_fused(fa, T, maxrows, C.st);
     ++C.launches;
+    if (dprof) {
+      std::vector<long long> hp((size_t)T * 8);
+      TLRG_CUDA(cudaMemcpyAsync(hp.data(), dprof, sizeof(long long) * T * 8,
+                                cudaMemcpyDeviceToHost, C.st));
+      C.wait();
+      int w = 0;
+      for (int s2 = 1; s2 < T; ++s2)
+        if (hp[8 * s2 + 6] > hp[8 * w + 6]) w = s2;
+      long long tot = 0, rds = 0;
+      for (int s2 = 0; s2 < T; ++s2) {
+        tot += hp[8 * s2 + 6];
+        rds += hp[8 * s2 + 7];
+      }
+      std::fprintf(stderr,
+                   "fused T=%d K=%d slowest slot %d rounds %lld: draw %lld sample %lld tau %lld "
+                   "deflate %lld mgs %lld absorb %lld total %lld kcyc | mean rounds %.2f mean "
+                   "total %lld kcyc\n",
+                   T, fo.K, w, hp[8 * w + 7], hp[8 * w] / 1000, hp[8 * w + 1] / 1000,
+                   hp[8 * w + 2] / 1000, hp[8 * w + 3] / 1000, hp[8 * w + 4] / 1000,
+                   hp[8 * w + 5] / 1000, hp[8 * w + 6] / 1000, (double)rds / T, tot / T / 1000);
+    }
   } else {
   // ---- static per-column launch tables (staged before capture) ---------------
   std::vector<std::vector<GemmProblem>> stages;

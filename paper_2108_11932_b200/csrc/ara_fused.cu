@@ -23,9 +23,14 @@ namespace tlrg {
 
 namespace {
 
-constexpr int FT = 512;         // threads per CTA (one thread per tile row)
-constexpr int FW = FT / 32;     // warps
+constexpr int FT = 256;         // consumer threads per CTA
+constexpr int FW = FT / 32;     // consumer warps
+constexpr int FTP = FT + 32;    // + one producer warp (gaussian stream)
+
+// barrier among the consumer warps only (the producer warp runs free)
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(FT) : "memory"); }
 constexpr int MAXROWS = 512;
+constexpr int RPT = MAXROWS / FT;  // tile rows per consumer thread (r = tid + i*FT)
 constexpr int PART_UNITS = 16;  // split-k partial tiles kept in shared memory
 
 struct FSmem {
@@ -35,7 +40,7 @@ struct FSmem {
   double* Rt;     // bs x bs
   double* part;   // PART_UNITS x 64 x NT
   double* cbuf;   // bs (coefficients)
-  double* wpart;  // FW x 32 per-warp partial coefficient vectors
+  double* wpart;  // 2 x FW x 32 per-warp partial coefficient vectors
   double* wred;   // FW
   double* tiny;   // bs
   double* cn;     // bs
@@ -43,15 +48,14 @@ struct FSmem {
   double* recent; // window
   uint8_t* defi;  // bs
   int* keep;      // bs
-  GenSmem* gen;   // aliases Y
 };
 
 __device__ __forceinline__ double cta_sum(double v, double* wred) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_sum(v);
-  __syncthreads();
+  cbar();
   if (lane == 0) wred[warp] = v;
-  __syncthreads();
+  cbar();
   double s = 0.0;
 #pragma unroll
   for (int w = 0; w < FW; ++w) s += wred[w];
@@ -76,6 +80,60 @@ __device__ void tn16(int M, int Kd, ACol acol, BCol bcol, Sgn sgn, Out out, doub
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int mtiles = (M + 7) / 8;
   if (mtiles == 0 || Kd <= 0) return;
+  if (mtiles >= FW) {
+    // wide: k-outer, MTW m-tiles per warp share each B fragment (more loads in flight)
+    constexpr int MTW = 4;
+    const int k8 = (Kd + 7) / 8;
+    const double* bp[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) bp[j] = bcol(j * 8 + g);
+    for (int base = 0; base < mtiles; base += FW * MTW) {
+      const double* ap[MTW];
+      bool mv[MTW];
+#pragma unroll
+      for (int i = 0; i < MTW; ++i) {
+        const int m = (base + warp + FW * i) * 8 + g;
+        mv[i] = m < M;
+        ap[i] = mv[i] ? acol(m) : nullptr;
+      }
+      double acc[MTW][NT][2];
+#pragma unroll
+      for (int i = 0; i < MTW; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 2
+      for (int kb = 0; kb < k8; ++kb) {
+        const int kk = kb * 8 + 2 * t;
+        const bool kv = kk < Kd;
+        double2 b[NT], a[MTW];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) b[j] = kv ? ld2(bp[j] + kk) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < MTW; ++i) a[i] = (mv[i] && kv) ? ld2(ap[i] + kk) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < MTW; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+            dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < MTW; ++i) {
+        const int m = (base + warp + FW * i) * 8 + g;
+        if (m < M) {
+          const double sg = sgn(m);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            out(m, j * 8 + 2 * t, sg * acc[i][j][0]);
+            out(m, j * 8 + 2 * t + 1, sg * acc[i][j][1]);
+          }
+        }
+      }
+    }
+    cbar();
+    return;
+  }
   int ks = FW / mtiles;
   if (ks < 1) ks = 1;
   if (ks * mtiles > PART_UNITS) ks = PART_UNITS / mtiles > 0 ? PART_UNITS / mtiles : 1;
@@ -127,7 +185,7 @@ __device__ void tn16(int M, int Kd, ACol acol, BCol bcol, Sgn sgn, Out out, doub
     }
   }
   if (ks > 1) {
-    __syncthreads();
+    cbar();
     for (int e = threadIdx.x; e < mtiles * 64 * NT; e += FT) {
       const int mt = e / (64 * NT), r = e % (64 * NT);
       const int m = mt * 8 + r / (8 * NT), n = r % (8 * NT);
@@ -137,7 +195,7 @@ __device__ void tn16(int M, int Kd, ACol acol, BCol bcol, Sgn sgn, Out out, doub
       out(m, n, sgn(m) * sum);
     }
   }
-  __syncthreads();
+  cbar();
 }
 
 // epi(r, c, v): v = sum_{k<Kd} acol(k)[r] * B[k + c*ldb],  r < rows (even, <= 512),
@@ -203,7 +261,7 @@ __device__ void nn16(int rows, int Kd, ACol acol, const double* B, int ldb, Epi 
       }
     }
   }
-  __syncthreads();
+  cbar();
 }
 
 struct TileCtx {
@@ -211,6 +269,7 @@ struct TileCtx {
   GaussStreams G;
   int s, rows, cols, bs, ldy, q;
   long long* cur;  // smem cursor (absolute stream position)
+  long long* av;   // smem count of values produced (producer warp)
 };
 
 // Reduce-scatter of N (16 or 32) values over a warp: afterwards every lane
@@ -239,61 +298,95 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[N]) {
 }
 
 // one classical pass of column j of the register-resident panel against the
-// columns p < j (each thread owns one tile row); coefficients land in S.cbuf
-// and are added to Rp(:, j) when add_r.  Two CTA barriers.
+// columns p < j (each thread owns RPT tile rows).  Every warp writes its
+// reduce-scattered partial dots to shared memory (double-buffered by pass
+// parity), ONE barrier, then lane p of every warp sums coefficient p over the
+// warps in a fixed order and the update takes it by shuffle.  Warp 0 adds the
+// coefficients to Rp(:, j) when rpj != null.
 template <int BS, int J>
-__device__ __forceinline__ void cgs_pass_reg(double (&y)[BS], FSmem& S, double* rpj) {
+__device__ __forceinline__ void cgs_pass_reg(double (&y)[RPT][BS], FSmem& S, double* rpj,
+                                             int& par) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int N = J <= 16 ? 16 : 32;
   double part[N];
 #pragma unroll
-  for (int p = 0; p < N; ++p) part[p] = p < J ? y[p] * y[J] : 0.0;
+  for (int p = 0; p < N; ++p) {
+    double v = 0.0;
+    if (p < J) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) v += y[i][p] * y[i][J];
+    }
+    part[p] = v;
+  }
   const double red = warp_reduce_scatter<N>(part);
+  double* wp = S.wpart + par * (FW * 32);
+  par ^= 1;
   if (N == 32) {
-    S.wpart[warp * 32 + lane] = red;
+    wp[warp * 32 + lane] = red;
   } else if ((lane & 1) == 0) {
-    S.wpart[warp * 32 + (lane >> 1)] = red;
+    wp[warp * 32 + (lane >> 1)] = red;
   }
-  __syncthreads();
-  if ((int)threadIdx.x < J) {
-    double c = 0.0;
+  cbar();
+  double c = 0.0;
+  if (lane < J) {
+    double h0 = 0.0, h1 = 0.0;
 #pragma unroll
-    for (int w = 0; w < FW; ++w) c += S.wpart[w * 32 + threadIdx.x];
-    S.cbuf[threadIdx.x] = c;
-    if (rpj) rpj[threadIdx.x] += c;
+    for (int w = 0; w < FW; w += 2) {
+      h0 += wp[w * 32 + lane];
+      h1 += wp[(w + 1) * 32 + lane];
+    }
+    c = h0 + h1;
   }
-  __syncthreads();
-  double acc = 0.0;
+  if (rpj && warp == 0 && lane < J) rpj[lane] += c;
+  double cf[J > 0 ? J : 1];
 #pragma unroll
-  for (int p = 0; p < J; ++p) acc += S.cbuf[p] * y[p];
-  y[J] -= acc;
+  for (int p = 0; p < J; ++p) cf[p] = __shfl_sync(0xffffffffu, c, p);
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int p = 0; p < J; p += 4) {
+      a0 += cf[p] * y[i][p];
+      if (p + 1 < J) a1 += cf[p + 1] * y[i][p + 1];
+      if (p + 2 < J) a2 += cf[p + 2] * y[i][p + 2];
+      if (p + 3 < J) a3 += cf[p + 3] * y[i][p + 3];
+    }
+    y[i][J] -= (a0 + a1) + (a2 + a3);
+  }
 }
 
-__device__ __forceinline__ double cta_norm(double v, FSmem& S) {
+// ||column||_2 over the tile rows of all consumer threads (one barrier)
+template <int BS>
+__device__ __forceinline__ double cta_norm(const double (&y)[RPT][BS], int J, FSmem& S, int& par) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum(v * v);
-  if (lane == 0) S.wred[warp] = v;
-  __syncthreads();
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) v += y[i][J] * y[i][J];
+  v = warp_sum(v);
+  double* wr = S.wpart + par * (FW * 32);  // shares the pass buffers' parity
+  par ^= 1;
+  if (lane == 0) wr[warp] = v;
+  cbar();
   double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < FW; ++w) s += S.wred[w];
+  for (int w = 0; w < FW; ++w) s += wr[w];
   return sqrt(s);
 }
 
 // panel MGS2 of one sweep (dense_kernels.cpp:331-375) with the panel held in
-// registers (row r of the tile in thread r); Rp is accumulated, deficient
-// columns are replaced from the tile's stream and projected against Q and the
-// earlier panel columns.
+// registers (rows tid + i*FT of the tile in thread tid); Rp is accumulated,
+// deficient columns are replaced from the tile's stream and projected against
+// Q and the earlier panel columns.
 template <int BS, int J>
-__device__ __forceinline__ void mgs_column(TileCtx& T, FSmem& S, double (&y)[BS], double tau) {
-  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
-  const bool rv = r < T.rows;
+__device__ __forceinline__ void mgs_column(TileCtx& T, FSmem& S, double (&y)[RPT][BS], double tau,
+                                           int& par) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* rpj = S.Rp + J * BS;
   if (J > 0) {
-    cgs_pass_reg<BS, J>(y, S, rpj);
-    cgs_pass_reg<BS, J>(y, S, rpj);
+    cgs_pass_reg<BS, J>(y, S, rpj, par);
+    cgs_pass_reg<BS, J>(y, S, rpj, par);
   }
-  double nj = cta_norm(y[J], S);
+  double nj = cta_norm<BS>(y, J, S, par);
   if (!(nj >= tau)) {
     if (threadIdx.x == 0 && !S.defi[J]) {
       S.defi[J] = 1;
@@ -301,80 +394,107 @@ __device__ __forceinline__ void mgs_column(TileCtx& T, FSmem& S, double (&y)[BS]
     }
     // fresh direction from the tile's own stream: y <- g - Q (Q^T g)
     const long long c0 = *T.cur;
-    __syncthreads();
+    {
+      volatile long long* av = T.av;
+      while (*av < c0 + T.rows) __nanosleep(64);
+      __threadfence_block();
+    }
+    cbar();
     if (threadIdx.x == 0) *T.cur = c0 + T.rows;
     const double* gb = T.G.buf + (long long)T.s * T.G.cap;
-    y[J] = rv ? gb[(c0 + r) % T.G.cap] : 0.0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = threadIdx.x + i * FT;
+      y[i][J] = r < T.rows ? gb[(c0 + r) % T.G.cap] : 0.0;
+    }
     const int q = T.q;
     if (q > 0) {
       const FusedSlot& sl = *T.sl;
       double* yj = S.Y + (long long)J * T.ldy;
-      if (rv) yj[r] = y[J];
-      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int r = threadIdx.x + i * FT;
+        if (r < T.rows) yj[r] = y[i][J];
+      }
+      cbar();
       for (int tq = warp; tq < q; tq += FW) {
         const double* qt = sl.Q + (long long)tq * T.rows;
         double s = 0.0;
-        for (int i = lane; i < T.rows; i += 32) s += qt[i] * yj[i];
+        for (int i2 = lane; i2 < T.rows; i2 += 32) s += qt[i2] * yj[i2];
         s = warp_sum(s);
         if (lane == 0) sl.repC[tq] = s;
       }
-      __syncthreads();
-      if (rv) {
-        double s = 0.0;
-        for (int tq = 0; tq < q; ++tq) s += sl.Q[(long long)tq * T.rows + r] * sl.repC[tq];
-        y[J] -= s;
+      cbar();
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int r = threadIdx.x + i * FT;
+        if (r < T.rows) {
+          double s = 0.0;
+          for (int tq = 0; tq < q; ++tq) s += sl.Q[(long long)tq * T.rows + r] * sl.repC[tq];
+          y[i][J] -= s;
+        }
       }
     }
     if (J > 0) {
-      cgs_pass_reg<BS, J>(y, S, nullptr);
-      cgs_pass_reg<BS, J>(y, S, nullptr);
+      cgs_pass_reg<BS, J>(y, S, nullptr, par);
+      cgs_pass_reg<BS, J>(y, S, nullptr, par);
     }
-    __syncthreads();  // wred reuse
-    nj = cta_norm(y[J], S);
+    nj = cta_norm<BS>(y, J, S, par);
     if (nj == 0.0) {
-      y[J] = (r == J % T.rows) ? 1.0 : 0.0;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) y[i][J] = (threadIdx.x + i * FT == J % T.rows) ? 1.0 : 0.0;
       nj = 1.0;
     }
     if (threadIdx.x == 0) rpj[J] = 0.0;
   } else {
     if (threadIdx.x == 0) rpj[J] = nj;
   }
-  y[J] *= 1.0 / nj;
+  const double inv = 1.0 / nj;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) y[i][J] *= inv;
 }
 
 template <int BS, int J>
 struct MgsUnroll {
-  __device__ __forceinline__ static void run(TileCtx& T, FSmem& S, double (&y)[BS], double tau) {
-    mgs_column<BS, J>(T, S, y, tau);
-    MgsUnroll<BS, J + 1>::run(T, S, y, tau);
+  __device__ __forceinline__ static void run(TileCtx& T, FSmem& S, double (&y)[RPT][BS],
+                                             double tau, int& par) {
+    mgs_column<BS, J>(T, S, y, tau, par);
+    MgsUnroll<BS, J + 1>::run(T, S, y, tau, par);
   }
 };
 template <int BS>
 struct MgsUnroll<BS, BS> {
-  __device__ __forceinline__ static void run(TileCtx&, FSmem&, double (&)[BS], double) {}
+  __device__ __forceinline__ static void run(TileCtx&, FSmem&, double (&)[RPT][BS], double, int&) {}
 };
 
 template <int NT>
 __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
   constexpr int BS = NT * 8;
-  const int r = threadIdx.x;
-  const bool rv = r < T.rows;
   for (int e = threadIdx.x; e < BS * BS; e += FT) S.Rp[e] = 0.0;
   if (sweep == 0)
     for (int j = threadIdx.x; j < BS; j += FT) {
       S.defi[j] = 0;
       S.tiny[j] = 0.0;
     }
-  double y[BS];
+  double y[RPT][BS];
 #pragma unroll
-  for (int c = 0; c < BS; ++c) y[c] = rv ? S.Y[r + c * T.ldy] : 0.0;
-  __syncthreads();
-  MgsUnroll<BS, 0>::run(T, S, y, tau);
-  if (rv) {
+  for (int i = 0; i < RPT; ++i) {
+    const int r = threadIdx.x + i * FT;
 #pragma unroll
-    for (int c = 0; c < BS; ++c) S.Y[r + c * T.ldy] = y[c];
+    for (int c = 0; c < BS; ++c) y[i][c] = r < T.rows ? S.Y[r + c * T.ldy] : 0.0;
   }
-  __syncthreads();
+  cbar();
+  int par = 0;
+  MgsUnroll<BS, 0>::run(T, S, y, tau, par);
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = threadIdx.x + i * FT;
+    if (r < T.rows) {
+#pragma unroll
+      for (int c = 0; c < BS; ++c) S.Y[r + c * T.ldy] = y[i][c];
+    }
+  }
+  cbar();
   // R <- Rp R   (R = I before the first sweep)
   const int w = BS;
   if (sweep == 0) {
@@ -386,14 +506,101 @@ __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
       for (int tt = p; tt <= jj; ++tt) sum += S.Rp[p + tt * w] * S.R[tt + jj * w];
       S.Rt[e] = p <= jj ? sum : 0.0;
     }
-    __syncthreads();
+    cbar();
     for (int e = threadIdx.x; e < w * w; e += FT) S.R[e] = S.Rt[e];
   }
-  __syncthreads();
+  cbar();
+}
+
+// ---- producer warp: the tile's exact tlr::Rng gaussian stream -------------
+// Runs concurrently with the consumer warps, keeping the ring buffer ahead of
+// the consumption cursor (Marsaglia polar pairs of mt19937_64 draws,
+// util.hpp:24-53, the same sequence cta_generate appends).  Publishes the
+// produced count through shared memory after a block-scope fence.
+constexpr int PQ = 128;  // polar pairs per producer batch
+struct ProdSmem {
+  uint64_t mt[MT_N];
+  double pu[PQ], pv[PQ], pq[PQ];
+};
+__device__ void stream_producer(const FusedArgs& A, int s, volatile long long* s_rel,
+                                volatile long long* s_av, volatile int* s_stop, ProdSmem& P) {
+  const int lane = threadIdx.x & 31;
+  RngState* g = &A.G.st[s];
+  double* buf = A.G.buf + (long long)s * A.G.cap;
+  const long long cap = A.G.cap;
+  for (int i = lane; i < MT_N; i += 32) P.mt[i] = g->mt[i];
+  int idx = g->idx;
+  long long have = *s_av;
+  __syncwarp();
+  while (!*s_stop) {
+    const long long rel = *s_rel;  // everything before it is consumed and released
+    long long room = cap - (have - rel);
+    if (room < 2 * PQ) {
+      __nanosleep(200);
+      continue;
+    }
+    // accept PQ polar pairs (cheap integer/FP work, ballot-compacted into smem)
+    int got = 0;
+    while (got < PQ) {
+      if (idx >= MT_N) {
+        warp_mt_twist(P.mt);
+        idx = 0;
+      }
+      int n_att = (MT_N - idx) / 2;
+      if (n_att > 32) n_att = 32;
+      bool acc = false;
+      double u = 0.0, v = 0.0, q = 0.0;
+      if (lane < n_att) {
+        u = 2.0 * mt_uniform(mt_temper(P.mt[idx + 2 * lane])) - 1.0;
+        v = 2.0 * mt_uniform(mt_temper(P.mt[idx + 2 * lane + 1])) - 1.0;
+        q = u * u + v * v;
+        acc = (q < 1.0) && (q != 0.0);
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, acc);
+      const int rank = __popc(mask & ((1u << lane) - 1u));
+      const int nacc = __popc(mask), left = PQ - got;
+      if (acc && rank < left) {
+        P.pu[got + rank] = u;
+        P.pv[got + rank] = v;
+        P.pq[got + rank] = q;
+      }
+      if (nacc >= left) {
+        unsigned m2 = mask;
+        for (int t = 0; t < left - 1; ++t) m2 &= m2 - 1;
+        idx += 2 * __ffs(m2);
+        got = PQ;
+      } else {
+        idx += 2 * n_att;
+        got += nacc;
+      }
+    }
+    __syncwarp();
+    // transform: PQ / 32 independent pairs per lane (log / sqrt latency overlapped)
+#pragma unroll
+    for (int i = 0; i < PQ / 32; ++i) {
+      const int e = lane + 32 * i;
+      const double q = P.pq[e];
+      const double f = sqrt(-2.0 * log(q) / q);
+      const long long p0 = (have + 2LL * e) % cap;  // pairs never straddle the wrap
+      buf[p0] = P.pu[e] * f;
+      buf[p0 + 1] = P.pv[e] * f;
+    }
+    have += 2LL * PQ;
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) *s_av = have;
+  }
+  __syncwarp();
+  for (int i = lane; i < MT_N; i += 32) g->mt[i] = P.mt[i];
+  if (lane == 0) {
+    g->idx = idx;
+    g->have_cached = 0;
+    A.G.avail[s] = have;
+  }
 }
 
 template <int NT>
-__global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
+__global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
   extern __shared__ __align__(16) double fsm[];
   const int s = blockIdx.x;
   const FusedSlot& sl = A.slots[s];
@@ -404,13 +611,12 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
     double* p = fsm;
     S.Y = p;
     p += A.ysz;
-    S.gen = reinterpret_cast<GenSmem*>(S.Y);
     S.R = p; p += bs * bs;
     S.Rp = p; p += bs * bs;
     S.Rt = p; p += bs * bs;
     S.part = p; p += PART_UNITS * 64 * NT;
     S.cbuf = p; p += bs;
-    S.wpart = p; p += FW * 32;
+    S.wpart = p; p += 2 * FW * 32;
     S.wred = p; p += FW;
     S.tiny = p; p += bs;
     S.cn = p; p += bs;
@@ -419,12 +625,15 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
     S.keep = reinterpret_cast<int*>(p); p += bs;
     S.defi = reinterpret_cast<uint8_t*>(p);
   }
-  __shared__ long long s_cur, s_av;
-  __shared__ int s_q, s_done, s_nkeep, s_rounds, s_conv, s_rcount, s_rpos;
+  __shared__ long long s_cur, s_av, s_rel;
+  __shared__ int s_q, s_done, s_nkeep, s_rounds, s_conv, s_rcount, s_rpos, s_stop;
   __shared__ double s_tau;
+  __shared__ ProdSmem prod;
   if (threadIdx.x == 0) {
     s_cur = A.G.cursor[s];
     s_av = A.G.avail[s];
+    s_rel = s_cur;
+    s_stop = 0;
     s_q = 0;
     s_done = sl.cap <= 0;
     s_rounds = 0;
@@ -433,24 +642,36 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
     s_rpos = 0;
   }
   __syncthreads();
-  TileCtx T{&sl, A.G, s, rows, cols, bs, ldy, 0, &s_cur};
+  if (threadIdx.x >= FT) {
+    stream_producer(A, s, &s_rel, &s_av, &s_stop, prod);
+    return;
+  }
+  TileCtx T{&sl, A.G, s, rows, cols, bs, ldy, 0, &s_cur, &s_av};
   const double* gb = A.G.buf + (long long)s * A.G.cap;
   const int kA = sl.kA, K = A.K, KW = kA + K;
   const int ldw = (KW + 1) & ~1;
 
+  long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_prev = clock64(), t_begin = t_prev;
+  auto tick = [&](int slot) {
+    if (A.prof && threadIdx.x == 0) {
+      const long long t = clock64();
+      pc[slot] += t - t_prev;
+      t_prev = t;
+    }
+  };
   while (!s_done && s_rounds < A.max_rounds) {
     // ---- draw: make sure Omega and every possible replacement are available
     const double* Om;
     {
-      const long long need = (long long)cols * bs + 2LL * bs * rows;
-      if (s_av - s_cur < need) {
-        long long want = s_cur + need + 2LL * cols * bs;
-        long long tgt = want < s_cur + A.G.cap ? want : s_cur + A.G.cap;
-        tgt &= ~1LL;
-        GaussStreams G = A.G;
-        cta_generate(G, s, s_av, tgt, *S.gen);
-        if (threadIdx.x == 0) s_av = A.G.avail[s];
-        __syncthreads();
+      const long long need = (long long)cols * bs;  // replacements wait on demand
+      {
+        // the previous round is complete: release its values to the producer
+        if (threadIdx.x == 0) *(volatile long long*)&s_rel = s_cur;
+        volatile long long* av = &s_av;
+        const long long c0 = s_cur;
+        while (*av - c0 < need) __nanosleep(64);
+        __threadfence_block();
       }
       const long long cur = s_cur, n = (long long)cols * bs;
       const long long start = cur % A.G.cap;
@@ -460,9 +681,10 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
         ring_copy(gb, A.G.cap, cur, n, sl.Om, FT);
         Om = sl.Om;
       }
-      __syncthreads();
+      cbar();
       if (threadIdx.x == 0) s_cur = cur + n;
     }
+    tick(0);
     // ---- sample -------------------------------------------------------------
     if (sl.Ad) {
       // dense operator: Y = A_tile Omega
@@ -483,12 +705,13 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
           [&](int k) { return k < kA ? sl.UA + (long long)k * rows : sl.H + (long long)(k - kA) * rows; },
           sl.W, ldw, [&](int m, int n, double v) { S.Y[m + n * ldy] = v; });
     }
+    tick(1);
     // ---- orthog (dense_kernels.cpp:379-420) ------------------------------------
     {
       double f = 0.0;
-      if (threadIdx.x < rows)
+      for (int r = threadIdx.x; r < rows; r += FT)
         for (int c = 0; c < bs; ++c) {
-          const double y = S.Y[threadIdx.x + c * ldy];
+          const double y = S.Y[r + c * ldy];
           f += y * y;
         }
       f = cta_sum(f, S.wred);
@@ -496,9 +719,10 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
         double tau = 100.0 * DBL_EPSILON * sqrt(f);
         s_tau = tau == 0.0 ? DBL_MIN : tau;
       }
-      __syncthreads();
+      cbar();
     }
     T.q = s_q;
+    tick(2);
     for (int sweep = 0; sweep < 2; ++sweep) {
       if (T.q > 0) {
         const int q = T.q, ldc = (q + 1) & ~1;
@@ -512,7 +736,9 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
             rows, q, [&](int k) { return sl.Q + (long long)k * rows; }, sl.Cq, ldc,
             [&](int m, int n, double v) { S.Y[m + n * ldy] -= v; });
       }
+      tick(3);
       panel_sweep<NT>(T, S, sweep, s_tau);
+      tick(4);
     }
     // ---- finalize + absorb (ara.cpp:171-195) -----------------------------------
     for (int jj = threadIdx.x; jj < bs; jj += FT) {
@@ -526,7 +752,7 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
         S.nm[jj] = fabs(S.R[jj + jj * bs]);
       }
     }
-    __syncthreads();
+    cbar();
     if (threadIdx.x == 0) {
       const int qc = s_q;
       int cnt = s_rcount, pos = s_rpos;
@@ -549,7 +775,7 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
       s_done = s_conv || (qc + nk) >= sl.cap;
       ++s_rounds;
     }
-    __syncthreads();
+    cbar();
     {
       const int nk = s_nkeep, q0 = s_q - s_nkeep;
       for (int e = threadIdx.x; e < nk * rows; e += FT) {
@@ -557,26 +783,30 @@ __global__ void __launch_bounds__(FT, 1) ara_fused_kernel(FusedArgs A) {
         sl.Q[(long long)(q0 + c) * rows + r] = S.Y[r + S.keep[c] * ldy];
       }
     }
-    __syncthreads();
+    cbar();
+    tick(5);
+  }
+  if (threadIdx.x == 0) *(volatile int*)&s_stop = 1;
+  if (A.prof && threadIdx.x == 0) {
+    pc[6] = clock64() - t_begin;
+    pc[7] = s_rounds;
+    for (int i = 0; i < 8; ++i) A.prof[8LL * s + i] = pc[i];
   }
   if (threadIdx.x == 0) {
     A.qcols[s] = s_q;
     A.rounds[s] = s_rounds;
     A.conv[s] = s_conv;
-    A.G.cursor[s] = s_cur;
-    A.G.avail[s] = s_av;
+    A.G.cursor[s] = s_cur;  // avail and the generator state: written by the producer
   }
 }
 
 size_t fused_smem_bytes(int maxrows, int bs, int window, int* ldy, long long* ysz) {
   int l = ((maxrows + 15) / 16) * 16 + 4;
   long long y = (long long)l * bs;
-  long long gen = (sizeof(GenSmem) + 7) / 8;
-  if (y < gen) y = gen;
   y = (y + 1) & ~1LL;
   *ldy = l;
   *ysz = y;
-  long long d = y + 3LL * bs * bs + (long long)PART_UNITS * 64 * (bs / 8) + bs + FW * 32 + FW +
+  long long d = y + 3LL * bs * bs + (long long)PART_UNITS * 64 * (bs / 8) + bs + 2 * FW * 32 + FW +
                 3LL * bs +
                 window + bs /*keep ints*/ + bs;
   return (size_t)d * 8 + 64;
@@ -611,7 +841,7 @@ void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st) {
   case NT * 8: {                                                                            \
     static size_t lim = enable_max_dyn_smem(ara_fused_kernel<NT>);                          \
     if (bytes > lim) throw CudaError("ara_fused: shared memory budget exceeded");           \
-    ara_fused_kernel<NT><<<T, FT, bytes, st>>>(args);                                       \
+    ara_fused_kernel<NT><<<T, FTP, bytes, st>>>(args);                                       \
     break;                                                                                  \
   }
     TLRG_FUSED_CASE(1)

@@ -177,6 +177,13 @@ std::vector<int> column_queue(const Matrix& M, int k) {
 
 void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPrep& P) {
   std::vector<int> queue = column_queue(M, k);
+  P.T = 0;
+  {
+    std::vector<int> rws;
+    for (int i : queue) rws.push_back(M.rows(i));
+    if (ara_fused_eligible(M.rows(k), rws, cfg.bs, cfg.window > 0 ? cfg.window : cfg.bs))
+      return;  // the fused ARA generates its streams in-kernel (producer warp)
+  }
   std::vector<uint64_t> seeds;
   int maxrows = 0;
   for (int i : queue) {

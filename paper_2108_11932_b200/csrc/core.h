@@ -266,6 +266,8 @@ struct StreamPrep {
     if (ev) cudaEventDestroy(ev);
   }
 };
+// the fused one-launch ARA applies (even tile sizes, shared-memory budget)
+bool ara_fused_eligible(int cols, const std::vector<int>& rows, int bs, int window);
 void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int bs, int maxrows,
                      int rounds_ahead, StreamPrep& P);
 void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,

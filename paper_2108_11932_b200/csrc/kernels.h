@@ -188,6 +188,7 @@ struct FusedArgs {
   int ldy;          // set by the launcher
   long long ysz;    // set by the launcher
   long long stg_half;  // set by the launcher
+  long long* prof;     // optional per-slot phase cycle counters (8 per slot)
 };
 bool ara_fused_supported(int maxrows, int bs, int window);
 void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st);
