@@ -231,33 +231,67 @@ def run_tlrg(args):
     os.environ.pop("TLRG_KTIMING", None)
     del F
 
-    # end-to-end through the C ABI with host buffers
-    diag, ranks, U, V = A0.to_parts()
+    # end-to-end through the C ABI with PINNED host buffers: upload A, factorize,
+    # download L (diag + U + V in the reference's flat layout) every step
     L = tg._lib
     lib = ctx.lib
     import ctypes as C
-    dg = np.ascontiguousarray(np.concatenate([d.T.ravel() for d in diag]))
-    Uf = np.ascontiguousarray(np.concatenate([u.T.ravel() for u in U]))
-    Vf = np.ascontiguousarray(np.concatenate([v.T.ravel() for v in V]))
-    rks = np.ascontiguousarray(ranks, dtype=np.int32)
-    h2d = dg.nbytes + Uf.nbytes + Vf.nbytes + rks.nbytes
+    nb_ = (n + b - 1) // b
+    rows_ = [min(b, n - i * b) for i in range(nb_)]
+    rks = np.ascontiguousarray(A0.ranks(), dtype=np.int32)
+
+    def flat_sizes(rk):
+        nd = sum(r * r for r in rows_)
+        nu = nv = 0
+        t = 0
+        for i in range(1, nb_):
+            for j in range(i):
+                nu += rows_[i] * int(rk[t])
+                nv += rows_[j] * int(rk[t])
+                t += 1
+        return nd, nu, nv
+
+    def pinned(count):
+        ptr = lib.tlrg_host_alloc(max(count, 1) * 8)
+        assert ptr, "tlrg_host_alloc failed"
+        arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(max(count, 1),))
+        return ptr, arr
+
+    nd, nu, nv = flat_sizes(rks)
+    bufs = [pinned(nd), pinned(nu), pinned(nv)]
+    stt = L.StatusC()
+    rc = lib.tlrg_matrix_download(A0.h, bufs[0][1].ctypes.data_as(L.dp),
+                                  bufs[1][1].ctypes.data_as(L.dp),
+                                  bufs[2][1].ctypes.data_as(L.dp), C.byref(stt))
+    assert rc == 0, stt.msg
+    F = factor(A0.copy(), cfg)
+    lnd, lnu, lnv = flat_sizes(F.L.ranks())
+    del F
+    obufs = [pinned(lnd), pinned(int(lnu * 1.05) + 4096), pinned(int(lnv * 1.05) + 4096)]
+    h2d = (nd + nu + nv) * 8 + rks.nbytes
     e2e_steps = max(1, min(args.steps, 3))
     e2e_t, d2h = [], 0
     for s in range(e2e_steps):
         barrier(dist)
         t0 = time.perf_counter()
         h = C.c_void_p()
-        stt = L.StatusC()
-        rc = lib.tlrg_matrix_upload(ctx.h, n, b, eps, dg.ctypes.data_as(L.dp),
-                                    rks.ctypes.data_as(L.ip), Uf.ctypes.data_as(L.dp),
-                                    Vf.ctypes.data_as(L.dp), C.byref(h), C.byref(stt))
+        rc = lib.tlrg_matrix_upload(ctx.h, n, b, eps, bufs[0][1].ctypes.data_as(L.dp),
+                                    rks.ctypes.data_as(L.ip), bufs[1][1].ctypes.data_as(L.dp),
+                                    bufs[2][1].ctypes.data_as(L.dp), C.byref(h), C.byref(stt))
         assert rc == 0, stt.msg
         Fm = factor(tg.TlrMatrix(h, ctx), cfg)
-        Ld, Lr, LU, LV = Fm.L.to_parts()
+        lh = lib.tlrg_factor_L(Fm.h)
+        rc = lib.tlrg_matrix_download(lh, obufs[0][1].ctypes.data_as(L.dp),
+                                      obufs[1][1].ctypes.data_as(L.dp),
+                                      obufs[2][1].ctypes.data_as(L.dp), C.byref(stt))
+        assert rc == 0, stt.msg
         e2e_t.append(time.perf_counter() - t0)
-        d2h = sum(x.nbytes for x in Ld) + sum(x.nbytes for x in LU) + sum(x.nbytes for x in LV)
+        lnd, lnu, lnv = flat_sizes(Fm.L.ranks())
+        d2h = (lnd + lnu + lnv) * 8
         del Fm
     e2e = allmax(dist, statistics.mean(e2e_t))
+    for ptr, _ in bufs + obufs:
+        lib.tlrg_host_free(ptr)
 
     peak = measure_fp64_peak() if rank == 0 else None
     cpu = None

@@ -173,6 +173,11 @@ int tlrg_gemm(tlrg_ctx ctx, int32_t M, int32_t N, int32_t K, int32_t transA, int
               double alpha, const double* A, const double* B, double beta, double* C,
               tlrg_status* st);
 
+/* Page-locked host buffers for the upload/download calls (cudaHostAlloc);
+ * transfers from/to them run at link speed.  NULL on failure. */
+void* tlrg_host_alloc(uint64_t bytes);
+void tlrg_host_free(void* p);
+
 /* Library version string and the sm target it was built for. */
 const char* tlrg_version(void);
 /* cudaProfilerStart/Stop, to scope ncu / nsys captures to a region */

@@ -52,6 +52,8 @@ class StatusC(C.Structure):
 # exported symbol -> (restype, argtypes); this table is also the export check
 SIGNATURES = {
     "tlrg_version": (C.c_char_p, []),
+    "tlrg_host_alloc": (C.c_void_p, [C.c_uint64]),
+    "tlrg_host_free": (None, [C.c_void_p]),
     "tlrg_profiler": (None, [C.c_int]),
     "tlrg_default_ara_config": (None, [C.POINTER(AraConfigC)]),
     "tlrg_default_workspace": (None, [C.POINTER(WorkspaceC)]),

@@ -403,6 +403,18 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     if (!S.Sref.empty()) cst.flops_ref += (double)bs * h_rounds[s] * S.Sref[s];
   }
   (void)h_flags_unused;
+  {
+    const char* fp = std::getenv("TLRG_FUSED_PROF");
+    if (fp && fp[0] == '1') {
+      int qm = 0;
+      long long qs = 0;
+      for (int s = 0; s < T; ++s) {
+        qm = std::max(qm, q[s]);
+        qs += q[s];
+      }
+      std::fprintf(stderr, "ara T=%d basis width max %d mean %.1f\n", T, qm, (double)qs / T);
+    }
+  }
 
   // ---- exit projection B = E^T Q (ara.cpp:380-387), all tiles at once ------
   Timer tp, tr;

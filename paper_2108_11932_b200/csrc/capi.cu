@@ -80,15 +80,20 @@ std::unique_ptr<Matrix> upload(Ctx& C, int64_t n, int b, double eps, const doubl
   M->U.assign(nt, nullptr);
   M->V.assign(nt, nullptr);
   TLRG_CUDA(cudaMalloc(&M->diag, sizeof(double) * (size_t)nb * b * b));
-  size_t off = 0;
-  for (int k = 0; k < nb; ++k) {
-    int r = M->rows(k);
-    if (diag)
-      TLRG_CUDA(cudaMemcpy(M->diag + (size_t)k * b * b, diag + off, sizeof(double) * r * r,
-                           cudaMemcpyHostToDevice));
-    else
-      TLRG_CUDA(cudaMemset(M->diag + (size_t)k * b * b, 0, sizeof(double) * r * r));
-    off += (size_t)r * r;
+  if (diag && n % b == 0) {
+    TLRG_CUDA(cudaMemcpyAsync(M->diag, diag, sizeof(double) * (size_t)nb * b * b,
+                              cudaMemcpyHostToDevice, C.st));
+  } else {
+    size_t off = 0;
+    for (int k = 0; k < nb; ++k) {
+      int r = M->rows(k);
+      if (diag)
+        TLRG_CUDA(cudaMemcpyAsync(M->diag + (size_t)k * b * b, diag + off, sizeof(double) * r * r,
+                                  cudaMemcpyHostToDevice, C.st));
+      else
+        TLRG_CUDA(cudaMemsetAsync(M->diag + (size_t)k * b * b, 0, sizeof(double) * r * r, C.st));
+      off += (size_t)r * r;
+    }
   }
   size_t totU = 0, totV = 0;
   for (int i = 1; i < nb; ++i)
@@ -102,8 +107,9 @@ std::unique_ptr<Matrix> upload(Ctx& C, int64_t n, int b, double eps, const doubl
   M->stores.push_back(S);
   double* dU = totU ? S->alloc(totU) : nullptr;
   double* dV = totV ? S->alloc(totV) : nullptr;
-  if (totU) TLRG_CUDA(cudaMemcpy(dU, U, sizeof(double) * totU, cudaMemcpyHostToDevice));
-  if (totV) TLRG_CUDA(cudaMemcpy(dV, V, sizeof(double) * totV, cudaMemcpyHostToDevice));
+  if (totU) TLRG_CUDA(cudaMemcpyAsync(dU, U, sizeof(double) * totU, cudaMemcpyHostToDevice, C.st));
+  if (totV) TLRG_CUDA(cudaMemcpyAsync(dV, V, sizeof(double) * totV, cudaMemcpyHostToDevice, C.st));
+  C.sync();
   size_t ou = 0, ov = 0;
   for (int i = 1; i < nb; ++i)
     for (int j = 0; j < i; ++j) {
@@ -120,33 +126,53 @@ std::unique_ptr<Matrix> upload(Ctx& C, int64_t n, int b, double eps, const doubl
   return M;
 }
 
+// Device-side gather of the tile payloads into the reference's flat layout,
+// then ONE device->host copy per stream (pinned host memory runs at link speed).
 void download(const Matrix& M, double* diag, double* U, double* V) {
+  Ctx& C = *M.ctx;
   const int nb = M.nb, b = M.b;
   if (diag) {
-    size_t off = 0;
-    for (int k = 0; k < nb; ++k) {
-      int r = M.rows(k);
-      TLRG_CUDA(cudaMemcpy(diag + off, M.diag + (size_t)k * b * b, sizeof(double) * r * r,
-                           cudaMemcpyDeviceToHost));
-      off += (size_t)r * r;
+    if (M.n % b == 0) {
+      TLRG_CUDA(cudaMemcpyAsync(diag, M.diag, sizeof(double) * (size_t)nb * b * b,
+                                cudaMemcpyDeviceToHost, C.st));
+    } else {
+      size_t off = 0;
+      for (int k = 0; k < nb; ++k) {
+        int r = M.rows(k);
+        TLRG_CUDA(cudaMemcpyAsync(diag + off, M.diag + (size_t)k * b * b, sizeof(double) * r * r,
+                                  cudaMemcpyDeviceToHost, C.st));
+        off += (size_t)r * r;
+      }
     }
   }
-  size_t ou = 0, ov = 0;
+  size_t tu = 0, tv = 0;
   for (int i = 1; i < nb; ++i)
     for (int j = 0; j < i; ++j) {
-      long long t = tri_index(i, j);
-      int r = M.rank[t];
-      if (r) {
-        if (U)
-          TLRG_CUDA(cudaMemcpy(U + ou, M.U[t], sizeof(double) * M.rows(i) * r,
-                               cudaMemcpyDeviceToHost));
-        if (V)
-          TLRG_CUDA(cudaMemcpy(V + ov, M.V[t], sizeof(double) * M.rows(j) * r,
-                               cudaMemcpyDeviceToHost));
-      }
-      ou += (size_t)M.rows(i) * r;
-      ov += (size_t)M.rows(j) * r;
+      int r = M.rank[tri_index(i, j)];
+      tu += (size_t)M.rows(i) * r;
+      tv += (size_t)M.rows(j) * r;
     }
+  if (U || V) {
+    double* su = (U && tu) ? C.buf<double>("dl_U", tu) : nullptr;
+    double* sv = (V && tv) ? C.buf<double>("dl_V", tv) : nullptr;
+    std::vector<CopyItem> cp;
+    size_t ou = 0, ov = 0;
+    for (int i = 1; i < nb; ++i)
+      for (int j = 0; j < i; ++j) {
+        long long t = tri_index(i, j);
+        int r = M.rank[t];
+        if (r) {
+          if (su) cp.push_back({M.U[t], su + ou, M.rows(i), M.rows(i), M.rows(i), r});
+          if (sv) cp.push_back({M.V[t], sv + ov, M.rows(j), M.rows(j), M.rows(j), r});
+        }
+        ou += (size_t)M.rows(i) * r;
+        ov += (size_t)M.rows(j) * r;
+      }
+    if (!cp.empty()) batched_copy(C.push(cp), (int)cp.size(), C.st);
+    if (su) TLRG_CUDA(cudaMemcpyAsync(U, su, sizeof(double) * tu, cudaMemcpyDeviceToHost, C.st));
+    if (sv) TLRG_CUDA(cudaMemcpyAsync(V, sv, sizeof(double) * tv, cudaMemcpyDeviceToHost, C.st));
+  }
+  C.sync();
 }
 
 std::unique_ptr<Matrix> clone(Ctx& C, const Matrix& M) {
@@ -212,6 +238,15 @@ void upload_d(DUpload& u, const Matrix& M, const double* dd, const double* de, c
 extern "C" {
 
 const char* tlrg_version(void) { return "tlrg 0.1 (sm_100a, FP64 DMMA)"; }
+
+void* tlrg_host_alloc(uint64_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+void tlrg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
 
 void tlrg_profiler(int on) {
   if (on) cudaProfilerStart();

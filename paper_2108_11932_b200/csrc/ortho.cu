@@ -57,7 +57,7 @@ void ara_absorb(AbsorbTask* d_tasks, int ntask, cudaStream_t st) {
 // ordering; a warp owns one column pair per step.  Works on a staged copy
 // (shared memory when it fits, else T.work) and writes the columns back sorted
 // by singular value (descending, ties by index) like dgesdd's output order.
-constexpr int JT = 256;
+constexpr int JT = 1024;
 
 __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int staged) {
   extern __shared__ double jsm[];

@@ -210,7 +210,7 @@ void panel_tau(PanelTask* d_tasks, int ntask, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------- PANEL MGS ---
-constexpr int PT = 128;
+constexpr int PT = 512;
 constexpr int PW = PT / 32;
 
 struct PanelSmem {
