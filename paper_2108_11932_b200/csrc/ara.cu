@@ -187,6 +187,10 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   for (int s = 0; s < T; ++s) capall = std::max(capall, S.cap[s]);
   const int max_rounds = 4 * capall + 8;  // a tile gains >= 1 column per round or converges
   Timer tm;
+  bool recomp_in_kernel = false;
+  double *Uo = nullptr, *Vo = nullptr;
+  int* rank_in = nullptr;
+  std::vector<int> h_rank_in(T, -1);
   std::vector<std::pair<cudaGraphExec_t, cudaGraph_t>> graph_cleanup;
   if (use_fused) {
     // ---- every round of every tile in ONE launch (one CTA per tile) ----------
@@ -196,8 +200,13 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     std::vector<long long> woff(T);
     for (int s = 0; s < T; ++s) {
       woff[s] = wtot;
-      wtot += (long long)((fo.Ad.empty() || !fo.Ad[s] ? fo.kA[s] + fo.K : 0) + 2) * bs;
+      wtot += (long long)((fo.Ad.empty() || !fo.Ad[s] ? fo.kA[s] + fo.K : 0) + 2) *
+              std::max(bs, FUSED_QMAX);
     }
+    recomp_in_kernel = cfg.recompress && (1.0 - 1.0 / cfg.safety) * cfg.eps > 0.0;
+    Uo = C.buf<double>("fusedUo", (size_t)T * maxrows * FUSED_QMAX);
+    Vo = C.buf<double>("fusedVo", (size_t)T * cols * FUSED_QMAX);
+    rank_in = C.buf<int>("fusedRank", (size_t)T);
     double* Wb = C.buf<double>("fusedW", (size_t)wtot);
     double* rc = C.buf<double>("fusedRC", (size_t)T * capmax);
     std::vector<FusedSlot> slots(T);
@@ -217,6 +226,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       f.W = Wb + woff[s];
       f.Cq = Cdef + (size_t)s * capmax * bs;
       f.repC = rc + (size_t)s * capmax;
+      f.Uo = Uo + (size_t)s * maxrows * FUSED_QMAX;
+      f.Vo = Vo + (size_t)s * cols * FUSED_QMAX;
     }
     FusedArgs fa{};
     fa.slots = C.push(slots);
@@ -232,6 +243,9 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     fa.qcols = qcols;
     fa.rounds = rounds;
     fa.conv = conv;
+    fa.recompress = recomp_in_kernel ? 1 : 0;
+    fa.cut = (1.0 - 1.0 / cfg.safety) * cfg.eps;
+    fa.rank_out = rank_in;
     const char* fp = std::getenv("TLRG_FUSED_PROF");
     long long* dprof = nullptr;
     if (fp && fp[0] == '1') {
@@ -381,6 +395,9 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
                             C.st));
   TLRG_CUDA(cudaMemcpyAsync(hcur.data(), G.cursor, sizeof(long long) * T, cudaMemcpyDeviceToHost,
                             C.st));
+  if (recomp_in_kernel)
+    TLRG_CUDA(cudaMemcpyAsync(h_rank_in.data(), rank_in, sizeof(int) * T, cudaMemcpyDeviceToHost,
+                              C.st));
   C.wait();
   for (auto& gc : graph_cleanup) {
     cudaGraphExecDestroy(gc.first);
@@ -416,6 +433,11 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     }
   }
 
+  // tiles recompressed in the fused kernel drop out of the batched path
+  std::vector<int> q_all = q;
+  if (recomp_in_kernel)
+    for (int s = 0; s < T; ++s)
+      if (h_rank_in[s] >= 0) q[s] = 0;
   // ---- exit projection B = E^T Q (ara.cpp:380-387), all tiles at once ------
   Timer tp, tr;
   tp.start(C.st);
@@ -426,7 +448,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     boff[s] = btot;
     btot += (long long)cols * q[s];
     qmax = std::max(qmax, q[s]);
-    if (!S.Sref.empty()) cst.flops_ref += q[s] * S.Sref[s];
+    if (!S.Sref.empty()) cst.flops_ref += q_all[s] * S.Sref[s];
   }
   double* Bb = C.buf<double>("B", (size_t)std::max(btot, 1LL));
   op.project(q, Q, Qstride, Bb, boff);
@@ -517,6 +539,9 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   } else {
     for (int s = 0; s < T; ++s) fr[s] = q[s];
   }
+  if (recomp_in_kernel)
+    for (int s = 0; s < T; ++s)
+      if (h_rank_in[s] >= 0) fr[s] = h_rank_in[s];
   // ---- final factors into one contiguous panel (in out_order) -------------
   long long utot = 0, vtot = 0;
   for (int s : out_order) {
@@ -537,7 +562,11 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     out.V[s] = Vp + vo;
     uo += (long long)S.rows[s] * fr[s];
     vo += (long long)cols * fr[s];
-    if (recomp) {
+    if (recomp_in_kernel && h_rank_in[s] >= 0) {
+      cpy.push_back({Uo + (size_t)s * maxrows * FUSED_QMAX, out.U[s], S.rows[s], S.rows[s],
+                     S.rows[s], fr[s]});
+      cpy.push_back({Vo + (size_t)s * cols * FUSED_QMAX, out.V[s], cols, cols, cols, fr[s]});
+    } else if (recomp) {
       // Q <- Q V_s ;  B <- Z (U_s sigma)
       GemmProblem g{};
       g.A = Q + s * Qstride; g.lda = S.rows[s];

@@ -48,6 +48,8 @@ struct FSmem {
   double* recent; // window
   uint8_t* defi;  // bs
   int* keep;      // bs
+  double* sig;    // FUSED_QMAX
+  int* perm;      // FUSED_QMAX
 };
 
 __device__ __forceinline__ double cta_sum(double v, double* wred) {
@@ -270,6 +272,7 @@ struct TileCtx {
   int s, rows, cols, bs, ldy, q;
   long long* cur;  // smem cursor (absolute stream position)
   long long* av;   // smem count of values produced (producer warp)
+  int wlim;        // panel columns actually present (<= BS)
 };
 
 // Reduce-scatter of N (16 or 32) values over a warp: afterwards every lane
@@ -380,6 +383,7 @@ __device__ __forceinline__ double cta_norm(const double (&y)[RPT][BS], int J, FS
 template <int BS, int J>
 __device__ __forceinline__ void mgs_column(TileCtx& T, FSmem& S, double (&y)[RPT][BS], double tau,
                                            int& par) {
+  if (J >= T.wlim) return;  // uniform
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* rpj = S.Rp + J * BS;
   if (J > 0) {
@@ -512,6 +516,82 @@ __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
   cbar();
 }
 
+// ---- in-CTA one-sided Jacobi SVD of the small core (svd_truncate, ----------
+// dense_kernels.cpp:422-454): A (n x n, ld n) <- U Sigma, V <- right vectors
+// (both unsorted); sig[] the column norms; perm[] orders them descending (ties
+// by index, like the batched kernel); returns #{sigma > cut}.
+__device__ int cta_jacobi_svd(double* A, double* V, double* sig, int* perm, int n, double cut,
+                              double* wred, int* flag) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < n * n; e += FT) V[e] = (e % n == e / n) ? 1.0 : 0.0;
+  double f = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += FT) f += A[e] * A[e];
+  f = cta_sum(f, wred);
+  const double tiny2 = f * 1e-34;
+  const double tol = fmax(1e-15, 2.0 * sqrt((double)n) * 2.220446049250313e-16);
+  const int nn = n + (n & 1);
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    cbar();
+    for (int step = 0; step < nn - 1; ++step) {
+      for (int pi = warp; pi < nn / 2; pi += FW) {
+        const int p = (step + pi) % (nn - 1);
+        const int q = pi == 0 ? nn - 1 : (step - pi + nn - 1) % (nn - 1);
+        if (p >= n || q >= n) continue;
+        double* ap = A + p * n;
+        double* aq = A + q * n;
+        double al = 0, be = 0, ga = 0;
+        for (int r = lane; r < n; r += 32) {
+          al += ap[r] * ap[r];
+          be += aq[r] * aq[r];
+          ga += ap[r] * aq[r];
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (al > tiny2 && be > tiny2 && fabs(ga) > tol * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+          for (int r = lane; r < n; r += 32) {
+            const double x = ap[r], y = aq[r];
+            ap[r] = c * x - sn * y;
+            aq[r] = sn * x + c * y;
+          }
+          double* vp = V + p * n;
+          double* vq = V + q * n;
+          for (int r = lane; r < n; r += 32) {
+            const double x = vp[r], y = vq[r];
+            vp[r] = c * x - sn * y;
+            vq[r] = sn * x + c * y;
+          }
+          if (lane == 0) *flag = 1;
+        }
+      }
+      cbar();
+    }
+    if (!*flag) break;
+    cbar();
+  }
+  for (int p = warp; p < n; p += FW) {
+    double v = 0.0;
+    for (int r = lane; r < n; r += 32) v += A[p * n + r] * A[p * n + r];
+    v = warp_sum(v);
+    if (lane == 0) sig[p] = sqrt(v);
+  }
+  cbar();
+  int cnt = 0;
+  for (int p = threadIdx.x; p < n; p += FT) {
+    const double sp = sig[p];
+    int rk = 0;
+    for (int q = 0; q < n; ++q) rk += (sig[q] > sp || (sig[q] == sp && q < p)) ? 1 : 0;
+    perm[rk] = p;
+  }
+  for (int p = 0; p < n; ++p) cnt += sig[p] > cut ? 1 : 0;
+  cbar();
+  return cnt;
+}
+
 // ---- producer warp: the tile's exact tlr::Rng gaussian stream -------------
 // Runs concurrently with the consumer warps, keeping the ring buffer ahead of
 // the consumption cursor (Marsaglia polar pairs of mt19937_64 draws,
@@ -599,30 +679,114 @@ __device__ void stream_producer(const FusedArgs& A, int s, volatile long long* s
   }
 }
 
+// ---- exit projection + SVD recompression of one converged tile ------------
+// (ara.cpp:380-398 and recompress_pair, ara.cpp:201-211), in the tile's CTA
+// while slower tiles are still sampling:
+//   B = E^T Q (cols x q) -> Z R = orthog(empty, B) (same panel MGS2, same stream)
+//   -> SVD of R cut at (1 - 1/eta) eps -> Uo = Q V_s, Vo = Z U_s sigma.
+template <int NTQ>
+__device__ int recompress_tile(const FusedArgs& A, const FusedSlot& sl, TileCtx& T, FSmem& S,
+                               int q, int* s_flag) {
+  constexpr int BSQ = NTQ * 8;
+  const int rows = sl.rows, cols = A.cols, ldy = T.ldy;
+  const int kA = sl.kA, KW = kA + A.K, ldw = (KW + 1) & ~1;
+  // projection into the smem panel (columns >= q hold don't-care values)
+  if (sl.Ad) {
+    tn16<NTQ>(
+        cols, rows, [&](int m) { return sl.Ad + (long long)m * sl.ldad; },
+        [&](int n) { return (const double*)(sl.Q + (long long)n * rows); }, [](int) { return 1.0; },
+        [&](int m, int n, double v) { S.Y[m + n * ldy] = v; }, S.part);
+  } else {
+    tn16<NTQ>(
+        KW, rows,
+        [&](int m) { return m < kA ? sl.UA + (long long)m * rows : sl.H + (long long)(m - kA) * rows; },
+        [&](int n) { return (const double*)(sl.Q + (long long)n * rows); },
+        [&](int m) { return m < kA ? 1.0 : -1.0; },
+        [&](int m, int n, double v) { sl.W[m + (long long)n * ldw] = v; }, S.part);
+    nn16<NTQ>(
+        cols, KW,
+        [&](int k) { return k < kA ? sl.VA + (long long)k * cols : A.Ucat + (long long)(k - kA) * cols; },
+        sl.W, ldw, [&](int m, int n, double v) { S.Y[m + n * ldy] = v; });
+  }
+  // orthog(empty, B): tau from the q real columns, two panel MGS2 sweeps
+  TileCtx T2 = T;
+  T2.rows = cols;
+  T2.q = 0;
+  T2.wlim = q;
+  __shared__ double s_tau2;
+  {
+    double f = 0.0;
+    for (int r = threadIdx.x; r < cols; r += FT)
+      for (int c = 0; c < q; ++c) f += S.Y[r + c * ldy] * S.Y[r + c * ldy];
+    f = cta_sum(f, S.wred);
+    if (threadIdx.x == 0) {
+      const double tau = 100.0 * DBL_EPSILON * sqrt(f);
+      s_tau2 = tau == 0.0 ? DBL_MIN : tau;
+    }
+    cbar();
+  }
+  panel_sweep<NTQ>(T2, S, 0, s_tau2);
+  panel_sweep<NTQ>(T2, S, 1, s_tau2);
+  // R (q x q, ld q) with the deficient-column convention of orthog
+  double* Ra = S.part;          // q x q
+  double* Va = S.part + q * q;  // q x q
+  for (int e = threadIdx.x; e < q * q; e += FT) {
+    const int i = e % q, j = e / q;
+    double v = S.R[i + j * BSQ];
+    if (S.defi[j]) v = (i == j) ? S.tiny[j] : 0.0;
+    Ra[e] = v;
+  }
+  cbar();
+  double* sig = S.sig;
+  int* perm = S.perm;
+  const int r = cta_jacobi_svd(Ra, Va, sig, perm, q, A.cut, S.wred, s_flag);
+  // Uo = Q V_s ; Vo = Z (U_s sigma)   (first r singular triplets, descending)
+  for (int e = threadIdx.x; e < rows * r; e += FT) {
+    const int row = e % rows, c = e / rows;
+    const double* v = Va + perm[c] * q;
+    double acc = 0.0;
+    for (int k = 0; k < q; ++k) acc += sl.Q[row + (long long)k * rows] * v[k];
+    sl.Uo[row + (long long)c * rows] = acc;
+  }
+  for (int e = threadIdx.x; e < cols * r; e += FT) {
+    const int row = e % cols, c = e / cols;
+    const double* u = Ra + perm[c] * q;
+    double acc = 0.0;
+    for (int k = 0; k < q; ++k) acc += S.Y[row + k * ldy] * u[k];
+    sl.Vo[row + (long long)c * cols] = acc;
+  }
+  cbar();
+  return r;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
   extern __shared__ __align__(16) double fsm[];
   const int s = blockIdx.x;
   const FusedSlot& sl = A.slots[s];
   const int rows = sl.rows, cols = A.cols, bs = NT * 8;
+  constexpr int BQ = NT * 8 > FUSED_QMAX ? NT * 8 : FUSED_QMAX;
   const int ldy = A.ldy;
   FSmem S;
   {
     double* p = fsm;
     S.Y = p;
     p += A.ysz;
-    S.R = p; p += bs * bs;
-    S.Rp = p; p += bs * bs;
-    S.Rt = p; p += bs * bs;
-    S.part = p; p += PART_UNITS * 64 * NT;
-    S.cbuf = p; p += bs;
+    S.R = p; p += BQ * BQ;
+    S.Rp = p; p += BQ * BQ;
+    S.Rt = p; p += BQ * BQ;
+    S.part = p; p += (PART_UNITS * 64 * NT > 2 * FUSED_QMAX * FUSED_QMAX
+                          ? PART_UNITS * 64 * NT : 2 * FUSED_QMAX * FUSED_QMAX);
+    S.cbuf = p; p += BQ;
     S.wpart = p; p += 2 * FW * 32;
     S.wred = p; p += FW;
-    S.tiny = p; p += bs;
-    S.cn = p; p += bs;
-    S.nm = p; p += bs;
+    S.tiny = p; p += BQ;
+    S.cn = p; p += BQ;
+    S.nm = p; p += BQ;
     S.recent = p; p += A.window;
-    S.keep = reinterpret_cast<int*>(p); p += bs;
+    S.keep = reinterpret_cast<int*>(p); p += BQ;
+    S.sig = p; p += FUSED_QMAX;
+    S.perm = reinterpret_cast<int*>(p); p += FUSED_QMAX;
     S.defi = reinterpret_cast<uint8_t*>(p);
   }
   __shared__ long long s_cur, s_av, s_rel;
@@ -646,7 +810,7 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
     stream_producer(A, s, &s_rel, &s_av, &s_stop, prod);
     return;
   }
-  TileCtx T{&sl, A.G, s, rows, cols, bs, ldy, 0, &s_cur, &s_av};
+  TileCtx T{&sl, A.G, s, rows, cols, bs, ldy, 0, &s_cur, &s_av, bs};
   const double* gb = A.G.buf + (long long)s * A.G.cap;
   const int kA = sl.kA, K = A.K, KW = kA + K;
   const int ldw = (KW + 1) & ~1;
@@ -786,6 +950,16 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
     cbar();
     tick(5);
   }
+  // ---- exit projection + recompression of this tile (q <= FUSED_QMAX) --------
+  __shared__ int s_flag;
+  if (A.recompress) {
+    const int q = s_q;
+    int rf = -1;
+    if (q == 0) rf = 0;
+    else if (q <= 16) rf = recompress_tile<2>(A, sl, T, S, q, &s_flag);
+    else if (q <= FUSED_QMAX) rf = recompress_tile<4>(A, sl, T, S, q, &s_flag);
+    if (threadIdx.x == 0) A.rank_out[s] = rf;
+  }
   if (threadIdx.x == 0) *(volatile int*)&s_stop = 1;
   if (A.prof && threadIdx.x == 0) {
     pc[6] = clock64() - t_begin;
@@ -802,13 +976,15 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
 
 size_t fused_smem_bytes(int maxrows, int bs, int window, int* ldy, long long* ysz) {
   int l = ((maxrows + 15) / 16) * 16 + 4;
-  long long y = (long long)l * bs;
+  long long y = (long long)l * std::max(bs, FUSED_QMAX);
   y = (y + 1) & ~1LL;
   *ldy = l;
   *ysz = y;
-  long long d = y + 3LL * bs * bs + (long long)PART_UNITS * 64 * (bs / 8) + bs + 2 * FW * 32 + FW +
-                3LL * bs +
-                window + bs /*keep ints*/ + bs;
+  const long long partn = std::max<long long>((long long)PART_UNITS * 64 * (bs / 8),
+                                              2LL * FUSED_QMAX * FUSED_QMAX);
+  const int bq = std::max(bs, FUSED_QMAX);
+  long long d = y + 3LL * bq * bq + partn + bq + 2 * FW * 32 + FW + 2 * FUSED_QMAX +
+                3LL * bq + window + bq /*keep ints*/ + bq;
   return (size_t)d * 8 + 64;
 }
 

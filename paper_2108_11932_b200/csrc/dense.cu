@@ -184,6 +184,95 @@ void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st) {
                                         st));
 }
 
+// ------------------------------------------------------------ CHOLQR -----
+// One pass of (shifted) Cholesky QR for a sketch Y (n x p) with G = Y^T Y:
+// R^T R = G + s I,  Rinv = R^{-1}  (s = 11 (n p + p (p + 1)) eps_mach tr(G) when
+// shift != 0, the shifted-CholQR3 bound).  Directions with a vanishing pivot
+// are dropped (zero column of Rinv), so a rank-deficient sketch yields zero
+// basis columns instead of a breakdown.  One CTA, p <= 160.
+__global__ void __launch_bounds__(1024) cholqr_kernel(const double* G, int p, int n, int shift,
+                                                      double* Rinv) {
+  extern __shared__ double csm[];
+  double* R = csm;              // p x p (row-major, ld p+1)
+  const int ld = p + 1;
+  __shared__ double s_tr;
+  __shared__ int s_dead[160];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < p * p; e += blockDim.x) {
+    const int i = e % p, j = e / p;
+    R[i * ld + j] = G[i + (long long)j * p];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < p; ++i) t += R[i * ld + i];
+    s_tr = t;
+  }
+  __syncthreads();
+  const double tr = s_tr;
+  if (shift) {
+    const double sh = 11.0 * ((double)n * p + (double)p * (p + 1)) * 2.220446049250313e-16 * tr;
+    for (int i = tid; i < p; i += blockDim.x) R[i * ld + i] += sh;
+  }
+  const double tol = 1e-24 * (tr > 0.0 ? tr : 1.0) / p;
+  __syncthreads();
+  // right-looking Cholesky, upper factor in place
+  for (int j = 0; j < p; ++j) {
+    const double d = R[j * ld + j];
+    const bool dead = !(d > tol);
+    __syncthreads();
+    if (tid == 0) s_dead[j] = dead;
+    if (dead) {
+      for (int k = tid; k < p; k += blockDim.x) {
+        R[j * ld + k] = 0.0;
+        R[k * ld + j] = 0.0;
+      }
+      __syncthreads();
+      continue;
+    }
+    const double rjj = sqrt(d);
+    for (int k = j + 1 + tid; k < p; k += blockDim.x) R[j * ld + k] /= rjj;
+    __syncthreads();
+    if (tid == 0) R[j * ld + j] = rjj;
+    const int m = p - j - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int a = j + 1 + e / m, b = j + 1 + e % m;
+      if (b >= a) R[a * ld + b] -= R[j * ld + a] * R[j * ld + b];
+    }
+    __syncthreads();
+  }
+  // Rinv: back substitution per column (one warp per column)
+  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < p; c += nw) {
+    // x_i for i = c .. 0 ; lane-parallel dot over k in (i, c]
+    double xs[5] = {0, 0, 0, 0, 0};  // lane holds x_k for k = lane + 32 t
+    for (int i = c; i >= 0; --i) {
+      double part = 0.0;
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        const int k = lane + 32 * t;
+        if (k > i && k <= c && k < p) part += R[i * ld + k] * xs[t];
+      }
+      const double sum = warp_sum(part);
+      const double rii = R[i * ld + i];
+      const double xi = (s_dead[i] || rii == 0.0) ? 0.0 : ((i == c ? 1.0 : 0.0) - sum) / rii;
+      if ((i & 31) == lane) xs[i >> 5] = xi;
+    }
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+      const int k = lane + 32 * t;
+      if (k < p) Rinv[k + (long long)c * p] = (k <= c) ? xs[t] : 0.0;
+    }
+  }
+}
+void cholqr_factor(const double* G, int p, int n, int shift, double* Rinv, cudaStream_t st) {
+  static size_t lim = enable_max_dyn_smem(cholqr_kernel);
+  (void)lim;
+  size_t bytes = (size_t)p * (p + 1) * 8;
+  cholqr_kernel<<<1, 1024, bytes, st>>>(G, p, n, shift, Rinv);
+  TLRG_CUDA(cudaGetLastError());
+}
+
 // ------------------------------------------------------- TRTRI (base) -----
 // X_bb = L_bb^{-1} for a list of diagonal blocks (<= 32 x 32), one CTA per
 // block, one warp per right-hand-side column (lane i owns row i).

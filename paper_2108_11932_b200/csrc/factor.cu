@@ -3,6 +3,7 @@
 //   Gram + H (dense phase) -> SYRK D_k -> Schur compensation -> POTRF / BK LDL
 //   -> dynamic-batched ARA -> panel TRSM (+perm, D^{-1}) -> pointer update.
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -233,9 +234,11 @@ bool modified_cholesky_device(Ctx& C, double* A, int n) {
 // consumed on the device (GEMM K from *rank), so the whole step enqueues without
 // a host round trip; the caller checks afterwards that at least 8 directions of
 // slack remained (r <= p - 8) and re-runs with a wider sketch otherwise.
+constexpr int kSchurMaxWidth = 160;  // sketch width cap (shared-memory Cholesky-QR)
 int schur_comp_width(int n, int rank_hint) {
   int p = std::max(32, rank_hint + 24);
   p = ((p + 7) / 8) * 8;
+  p = std::min(p, kSchurMaxWidth);
   return p > n ? n : p;
 }
 void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t seed, int p,
@@ -244,21 +247,10 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
   double* Y = C.buf<double>("sc_Y", (size_t)n * p);
   double* Bm = C.buf<double>("sc_B", (size_t)p * p);
   double* Vm = C.buf<double>("sc_V", (size_t)p * p);
-  double* R = C.buf<double>("sc_R", (size_t)p * p);
-  double* Rp = C.buf<double>("sc_Rp", (size_t)2 * p * p);
-  double* vec = C.buf<double>("sc_vec", (size_t)4 * p);
-  uint8_t* df = C.buf<uint8_t>("sc_def", (size_t)p);
   double* work = C.buf<double>("sc_work", (size_t)2 * p * p);
   double* sig = C.buf<double>("sc_sig", (size_t)p);
-  // replacement directions for rank-deficient sketch columns (not part of the
-  // reference's streams): a counter-based gaussian pool consumed by cursor
-  double* pool = C.buf<double>("sc_pool", (size_t)4 * n * p);
-  double* screp = C.buf<double>("sc_rep", (size_t)n * p);
-  long long* pcur = C.buf<long long>("sc_pcur", 1);
-  TLRG_CUDA(cudaMemsetAsync(pcur, 0, sizeof(long long), C.st));
-  fill_gaussian_philox(pool, 4LL * n * p, mix64(seed ^ 0x5c1ULL) + attempt, C.st);
   fill_gaussian_philox(Om, (long long)n * p, seed * 0x9E3779B97F4A7C15ULL + attempt, C.st);
-  C.launches += 3;
+  C.launches += 1;
   auto DtimesX = [&](const double* X, double* out) {
     std::vector<GemmProblem> pr(1);
     pr[0] = GemmProblem{};
@@ -266,19 +258,26 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
     pr[0].M = n; pr[0].N = p; pr[0].K = n; pr[0].alpha = 1.0;
     C.gemm(pr);
   };
+  // orthonormal basis of the sketch by shifted Cholesky-QR (3 passes; GEMMs +
+  // one tiny factor kernel each): X <- X R1^{-1} R2^{-1} R3^{-1}
+  double* Gq = C.buf<double>("sc_G", (size_t)p * p);
+  double* Ri = C.buf<double>("sc_Ri", (size_t)p * p);
+  double* Xt = C.buf<double>("sc_Xt", (size_t)n * p);
   auto orth = [&](double* X) {
-    std::vector<PanelTask> t(1);
-    PanelTask& P = t[0];
-    P = PanelTask{};
-    P.Y = X; P.Q = nullptr; P.R = R; P.Rp = Rp; P.tiny = vec; P.col_norms = vec + p;
-    P.new_mass = vec + 2 * p; P.deficient = df; P.gbuf = pool; P.gcursor = pcur;
-    P.rep = screp; P.repC = nullptr; P.gcap = 4LL * n * p;
-    P.rows = n; P.width = p; P.q = 0;
-    PanelTask* d = C.push(t);
-    panel_tau(d, 1, C.st);
-    panel_mgs(d, 1, 0, 0, p, n, C.st);
-    panel_mgs(d, 1, 1, 0, p, n, C.st);
-    C.launches += 3;
+    for (int pass = 0; pass < 3; ++pass) {
+      std::vector<GemmProblem> pr(1);
+      pr[0] = GemmProblem{};
+      pr[0].A = X; pr[0].lda = n; pr[0].transA = 1; pr[0].B = X; pr[0].ldb = n;
+      pr[0].C = Gq; pr[0].ldc = p; pr[0].M = p; pr[0].N = p; pr[0].K = n; pr[0].alpha = 1.0;
+      C.gemm(pr);
+      cholqr_factor(Gq, p, n, pass == 0, Ri, C.st);
+      ++C.launches;
+      pr[0] = GemmProblem{};
+      pr[0].A = X; pr[0].lda = n; pr[0].B = Ri; pr[0].ldb = p;
+      pr[0].C = Xt; pr[0].ldc = n; pr[0].M = n; pr[0].N = p; pr[0].K = p; pr[0].alpha = 1.0;
+      C.gemm(pr);
+      TLRG_CUDA(cudaMemcpyAsync(X, Xt, sizeof(double) * n * p, cudaMemcpyDeviceToDevice, C.st));
+    }
   };
   DtimesX(Om, Y);
   orth(Y);
@@ -334,8 +333,8 @@ void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint
     int* h = C.pinned_ints(1);
     TLRG_CUDA(cudaMemcpyAsync(h, rk, sizeof(int), cudaMemcpyDeviceToHost, C.st));
     C.wait();
-    if (h[0] > p - 8 && p < n) {
-      p = std::min(n, 2 * p);
+    if (h[0] > p - 8 && p < std::min(n, kSchurMaxWidth)) {
+      p = std::min(std::min(n, kSchurMaxWidth), 2 * p);
       continue;
     }
     rank_hint = h[0];
@@ -394,7 +393,10 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   Ev e0, e1, e4, e5, de0, de1, de2, de3, ejoin;
   StreamPrep prep;
 
+  const char* cpe = std::getenv("TLRG_COLPROF");
+  const bool colprof = cpe && cpe[0] == '1';
   for (int k = 0; k < nb; ++k) {
+    const auto t_col0 = std::chrono::steady_clock::now();
     const int rk = M.rows(k);
     double* diagk = M.diag + (size_t)k * b * b;
     // ---- gaussian streams of this column's ARA, generated on the side stream
@@ -487,7 +489,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     if (comp) TLRG_CUDA(cudaMemcpyAsync(hf, frob, sizeof(double), cudaMemcpyDeviceToHost, C.st));
     C.wait();
     int st_potrf = hs[0], st_sing = hs[1], st_rank = hs[2];
-    if (comp && st_rank > p_comp - 8 && p_comp < rk) {
+    if (comp && st_rank > p_comp - 8 && p_comp < std::min(rk, kSchurMaxWidth)) {
       // sketch too narrow for this column's spectrum: redo with a wider one
       rank_hint = 2 * p_comp;
       schur_compensation_device(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), corr,
@@ -554,6 +556,21 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     cudaEventRecord(e5.e, C.st);
     C.sync();
     S.t_misc += elapsed(e4, e5);
+    if (colprof) {
+      auto ms = [](Ev& a, Ev& b) {
+        float f = 0;
+        cudaEventElapsedTime(&f, a.e, b.e);
+        return f;
+      };
+      auto wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                               t_col0).count();
+      std::fprintf(stderr,
+                   "col %d T=%zu K=%d | setup %.3f diag %.3f (syrk %.3f comp %.3f fact %.3f) | "
+                   "ara %.3f proj %.3f recomp %.3f | join->end %.3f | dev %.3f host %.3f ms\n",
+                   k, res.size(), cs.K, ms(e0, e1), ms(de0, de3), ms(de0, de1), ms(de1, de2),
+                   ms(de2, de3), cst.t_sampling * 1e3, cst.t_projection * 1e3,
+                   cst.t_recompress * 1e3, ms(e4, e5), ms(e0, e5), wall_ms);
+    }
   }
   cudaEventRecord(d1.e, C.st);
   C.sync();

@@ -175,6 +175,8 @@ struct FusedSlot {
   double* W;     // (kA + K) x bs scratch
   double* Cq;    // cap x bs scratch
   double* repC;  // cap scratch
+  double* Uo;    // rows x QMAX recompressed U (Q V_s), written when recompressed in-kernel
+  double* Vo;    // cols x QMAX recompressed V before TRSM (Z U_s sigma)
 };
 struct FusedArgs {
   const FusedSlot* slots;
@@ -189,7 +191,11 @@ struct FusedArgs {
   long long ysz;    // set by the launcher
   long long stg_half;  // set by the launcher
   long long* prof;     // optional per-slot phase cycle counters (8 per slot)
+  int recompress;      // run the exit projection + SVD recompression in-kernel
+  double cut;          // (1 - 1/eta) eps
+  int* rank_out;       // final rank, or -1 when the tile needs the batched fallback
 };
+constexpr int FUSED_QMAX = 32;  // widest basis recompressed in-kernel
 bool ara_fused_supported(int maxrows, int bs, int window);
 void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st);
 
@@ -204,6 +210,8 @@ void sytrf_bk(double* A, int n, double* d, double* e, uint8_t* s2, int* perm, in
 void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
                 const double* d, const double* e, const uint8_t* s2, int* info,
                 cudaStream_t st);
+// (shifted) Cholesky-QR step: R^T R = G (+ shift), Rinv = R^{-1}, p <= 128
+void cholqr_factor(const double* G, int p, int n, int shift, double* Rinv, cudaStream_t st);
 // X_bb = L_bb^{-1} for diagonal blocks (offset, length <= 32) of an n x n lower L
 void trtri_base(const double* L, int n, double* X, const int* d_offs, const int* d_lens,
                 int nblocks, cudaStream_t st);
