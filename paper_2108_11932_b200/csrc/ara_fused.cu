@@ -549,10 +549,11 @@ __device__ int cta_jacobi_svd(double* A, double* V, double* sig, int* perm, int 
         al = warp_sum(al);
         be = warp_sum(be);
         ga = warp_sum(ga);
-        if (al > tiny2 && be > tiny2 && fabs(ga) > tol * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+        if (al > tiny2 && be > tiny2 && ga * ga > tol * tol * (al * be)) {
+          const double dl = be - al;
+          const double tt =
+              (dl >= 0 ? 2.0 * ga : -2.0 * ga) / (fabs(dl) + sqrt(dl * dl + 4.0 * ga * ga));
+          const double c = rsqrt(1.0 + tt * tt), sn = c * tt;
           for (int r = lane; r < n; r += 32) {
             const double x = ap[r], y = aq[r];
             ap[r] = c * x - sn * y;

@@ -42,9 +42,9 @@ __device__ __forceinline__ int chol32_reg(double (&v)[PB], int pw) {
       if (!(d > 0.0)) {
         fail = j;
       } else {
-        const double s = sqrt(d);
-        if (lane == j) v[j] = s;
-        else if (lane > j) v[j] /= s;
+        const double rs = rsqrt(d);
+        if (lane == j) v[j] = d * rs;
+        else if (lane > j) v[j] *= rs;
         const double lij = v[j];
 #pragma unroll
         for (int k = j + 1; k < PB; ++k) {
@@ -60,17 +60,17 @@ __device__ __forceinline__ int chol32_reg(double (&v)[PB], int pw) {
 __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int* info) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double Lp[PB][PB + 1];
+  __shared__ double Xp[PB][PB + 1];
   __shared__ double Ar[PB][PB + 1];
   __shared__ double Lb[PB][PB + 1];
   __shared__ int s_fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = (n + PB - 1) / PB;
   auto bw = [&](int t) { return min(PB, n - t * PB); };
-  const int gw = gridDim.x * PO_W;  // warps in the grid
   for (int p = 0; p < nt; ++p) {
     const int p0 = p * PB, pw = bw(p);
     const int below = n - (p0 + pw);
-    const bool mine = blockIdx.x == 0 || (int)blockIdx.x * PO_W < below;
+    const bool mine = blockIdx.x == 0 || (int)blockIdx.x * PO_T < below;
     // ---- phase 1 -------------------------------------------------------------
     if (mine) {
       if (warp == 0) {
@@ -87,21 +87,43 @@ __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int*
       if (s_fail >= 0) {
         if (tid == 0) atomicCAS(info, -1, p0 + s_fail);
       } else {
-        // L_rp = A_rp L_pp^{-T}: one warp per row, lane t owns x_t
-        for (int r = p0 + pw + blockIdx.x * PO_W + warp; r < n; r += gw) {
-          const double a = lane < pw ? A[r + (long long)(p0 + lane) * n] : 0.0;
-          double x = 0.0;
+        // X = L_pp^{-1} (lane j builds column j), then L_rp = A_rp X^T as a
+        // product: no per-row sequential substitution
+        if (warp == 0) {
+          double x[PB];
 #pragma unroll
-          for (int j = 0; j < PB; ++j) {
-            if (j < pw) {
-              const double part = lane < j ? x * Lp[j][lane] : 0.0;
-              const double sum = warp_sum(part);
-              const double aj = __shfl_sync(0xffffffffu, a, j);
-              const double xj = (aj - sum) / Lp[j][j];
-              if (lane == j) x = xj;
+          for (int i = 0; i < PB; ++i) x[i] = 0.0;
+          const int j = lane;
+          if (j < pw) {
+            x[j] = 1.0 / Lp[j][j];
+#pragma unroll
+            for (int i = 1; i < PB; ++i) {
+              if (i > j && i < pw) {
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < PB; ++k)
+                  if (k >= j && k < i) acc += Lp[i][k] * x[k];
+                x[i] = -acc / Lp[i][i];
+              }
             }
           }
-          if (lane < pw) A[r + (long long)(p0 + lane) * n] = x;
+#pragma unroll
+          for (int i = 0; i < PB; ++i) Xp[i][j] = x[i];  // Xp[i][j] = (L_pp^{-1})_{ij}
+        }
+        __syncthreads();
+        for (int r = p0 + pw + blockIdx.x * PO_T + tid; r < n; r += gridDim.x * PO_T) {
+          double a[PB];
+#pragma unroll
+          for (int t = 0; t < PB; ++t) a[t] = t < pw ? A[r + (long long)(p0 + t) * n] : 0.0;
+#pragma unroll
+          for (int jj = 0; jj < PB; ++jj) {
+            if (jj < pw) {
+              double acc = 0.0;
+#pragma unroll
+              for (int t = 0; t <= jj; ++t) acc += a[t] * Xp[jj][t];
+              A[r + (long long)(p0 + jj) * n] = acc;
+            }
+          }
         }
       }
     }

@@ -138,6 +138,8 @@ struct SvdTask {
   int m;        // rows of A (0 = n)
 };
 void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m = 0);
+// symmetric (PSD) core: A <- V diag(lam), V, |lam| sorted descending (n <= 160)
+void sym_jacobi(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st);
 
 // Block-diagonal product H[:, seg_j] = U_ij * G_ij for a set of (tile, j) items.
 struct BlockItem {

@@ -84,7 +84,9 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   __syncthreads();
   const double tiny2 = s_tiny;
   // rotation threshold: rounding level of an m-term dot product (dgesvj style)
-  const double tol = fmax(1e-15, 2.0 * sqrt((double)m) * 2.220446049250313e-16);
+  // rotation threshold: rounding level of an m-term dot product (m eps); a
+  // stricter one only makes the final sweeps chase rounding noise
+  const double tol = fmax(1e-15, (double)m * 2.220446049250313e-16);
   const int nn = n + (n & 1);
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) rotated = 0;
@@ -105,10 +107,12 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
         al = warp_sum(al);
         be = warp_sum(be);
         ga = warp_sum(ga);
-        if (al > tiny2 && be > tiny2 && fabs(ga) > tol * sqrt(al * be)) {
-          double zeta = (be - al) / (2.0 * ga);
-          double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        if (al > tiny2 && be > tiny2 && ga * ga > tol * tol * (al * be)) {
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+          // rewritten with one sqrt, one division and one rsqrt
+          const double dl = be - al;
+          double t = (dl >= 0 ? 2.0 * ga : -2.0 * ga) / (fabs(dl) + sqrt(dl * dl + 4.0 * ga * ga));
+          double c = rsqrt(1.0 + t * t), s = c * t;
           for (int r = lane; r < m; r += 32) {
             double x = ap[r], y = aq[r];
             ap[r] = c * x - s * y;
@@ -163,13 +167,265 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   if (tid == 0) *T.rank_out = cnt;
 }
 
+// ------------------------------------------- ONE-SIDED JACOBI (small) ------
+// Same algorithm and output as jacobi_svd for cores n <= 64 held in shared
+// memory, but instruction-lean: 256 threads, EIGHT lanes per column pair (4
+// pairs per warp, 3-level shuffle reductions), pair lists precomputed per
+// step.  The kernels on this path are issue-bound on a single SM.
+constexpr int JS_T = 256;
+__global__ void __launch_bounds__(JS_T) jacobi_small_kernel(SvdTask* tasks) {
+  extern __shared__ double jsm2[];
+  SvdTask& T = tasks[blockIdx.x];
+  const int n = T.n, m = T.m > 0 ? T.m : T.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = lane >> 3, l8 = lane & 7;  // pair slot within the warp, lane within the pair
+  if (n == 0) {
+    if (tid == 0) *T.rank_out = 0;
+    return;
+  }
+  double* A = jsm2;                        // m x n
+  double* V = A + (long long)m * n;        // n x n
+  for (int e = tid; e < m * n; e += JS_T) A[e] = T.A[e];
+  for (int e = tid; e < n * n; e += JS_T) V[e] = (e % n == e / n) ? 1.0 : 0.0;
+  __shared__ int rotated;
+  __shared__ double red[JS_T / 32];
+  {
+    double f = 0.0;
+    for (int e = tid; e < m * n; e += JS_T) f += A[e] * A[e];
+    f = warp_sum(f);
+    if (lane == 0) red[warp] = f;
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int w = 0; w < JS_T / 32; ++w) fro += red[w];
+  const double tiny2 = fro * 1e-34;
+  const double tol = fmax(1e-15, (double)m * 2.220446049250313e-16);
+  const int nn = n + (n & 1), np = nn / 2;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int step = 0; step < nn - 1; ++step) {
+      for (int base = warp * 4; base < np; base += (JS_T / 32) * 4) {
+        const int pi = base + sub;  // warp-uniform trip count (shuffles use the full mask)
+        int p = step + pi;
+        if (p >= nn - 1) p -= nn - 1;
+        int q = nn - 1;
+        if (pi != 0) {
+          q = step - pi;
+          if (q < 0) q += nn - 1;
+        }
+        const bool live = pi < np && p < n && q < n;
+        double al = 0, be = 0, ga = 0;
+        double* ap = A + (long long)p * m;
+        double* aq = A + (long long)q * m;
+        if (live)
+          for (int r = l8; r < m; r += 8) {
+            const double x = ap[r], y = aq[r];
+            al += x * x;
+            be += y * y;
+            ga += x * y;
+          }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (live && al > tiny2 && be > tiny2 && ga * ga > tol * tol * (al * be)) {
+          const double dl = be - al;
+          const double t = (dl >= 0 ? 2.0 * ga : -2.0 * ga) / (fabs(dl) + sqrt(dl * dl + 4.0 * ga * ga));
+          const double c = rsqrt(1.0 + t * t), sn = c * t;
+          for (int r = l8; r < m; r += 8) {
+            const double x = ap[r], y = aq[r];
+            ap[r] = c * x - sn * y;
+            aq[r] = sn * x + c * y;
+          }
+          double* vp = V + (long long)p * n;
+          double* vq = V + (long long)q * n;
+          for (int r = l8; r < n; r += 8) {
+            const double x = vp[r], y = vq[r];
+            vp[r] = c * x - sn * y;
+            vq[r] = sn * x + c * y;
+          }
+          if (l8 == 0) rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  for (int p = warp; p < n; p += JS_T / 32) {
+    double v = 0.0;
+    for (int r = lane; r < m; r += 32) v += A[(long long)p * m + r] * A[(long long)p * m + r];
+    v = warp_sum(v);
+    if (lane == 0) T.sig[p] = sqrt(v);
+  }
+  __syncthreads();
+  __shared__ int cnt;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  for (int p = warp; p < n; p += JS_T / 32) {
+    const double sp = T.sig[p];
+    int rk = 0;
+    for (int q = lane; q < n; q += 32) {
+      const double sq = T.sig[q];
+      rk += (sq > sp || (sq == sp && q < p)) ? 1 : 0;
+    }
+    rk = warp_sum_int(rk);
+    if (lane == 0 && sp > T.cut) atomicAdd(&cnt, 1);
+    for (int r = lane; r < m; r += 32) T.A[(long long)rk * m + r] = A[(long long)p * m + r];
+    for (int r = lane; r < n; r += 32) T.V[(long long)rk * n + r] = V[(long long)p * n + r];
+  }
+  __syncthreads();
+  for (int p = warp; p < n; p += JS_T / 32) {
+    double v = 0.0;
+    for (int r = lane; r < m; r += 32) v += T.A[(long long)p * m + r] * T.A[(long long)p * m + r];
+    v = warp_sum(v);
+    if (lane == 0) T.sig[p] = sqrt(v);
+  }
+  if (tid == 0) *T.rank_out = cnt;
+}
+
 void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m) {
   static size_t lim = enable_max_dyn_smem(jacobi_svd_kernel);
+  static size_t lim2 = enable_max_dyn_smem(jacobi_small_kernel);
   if (ntask <= 0) return;
   if (max_m <= 0) max_m = max_n;
   size_t bytes = ((size_t)max_m * max_n + (size_t)max_n * max_n) * 8;
+  if (max_n <= 128 && bytes <= lim2) {
+    jacobi_small_kernel<<<ntask, JS_T, bytes, st>>>(d_tasks);
+    TLRG_CUDA(cudaGetLastError());
+    return;
+  }
   int staged = bytes <= lim;
   jacobi_svd_kernel<<<ntask, JT, staged ? bytes : 16, st>>>(d_tasks, staged);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------- SYMMETRIC JACOBI ------
+// Two-sided cyclic Jacobi for a small symmetric matrix B (n x n, n <= 160):
+// B = V diag(lam) V^T.  Each parallel step applies n/2 disjoint rotations
+// (no dot products: the 2x2 blocks come straight from B), rows then columns,
+// three barriers per step.  Output in the SvdTask convention of jacobi_svd for
+// a symmetric PSD core: A <- V diag(lam), V, sig = |lam| sorted descending,
+// rank_out = #{|lam| > cut}.  Used by the Schur compensation's Rayleigh-Ritz.
+constexpr int SJ_T = 1024;
+__global__ void __launch_bounds__(SJ_T) sym_jacobi_kernel(SvdTask* tasks) {
+  extern __shared__ double sjm[];
+  SvdTask& T = tasks[blockIdx.x];
+  const int n = T.n, ld = n + 1;
+  double* B = sjm;              // n x ld (row-major)
+  double* V = B + n * ld;       // n x ld (row-major: V[k][col])
+  double* rc = V + n * ld;      // c per pair
+  double* rs = rc + 96;         // s per pair
+  int* rp = reinterpret_cast<int*>(rs + 96);
+  int* rq = rp + 96;
+  __shared__ int s_rot;
+  __shared__ double s_fro;
+  const int tid = threadIdx.x;
+  if (n == 0) {
+    if (tid == 0) *T.rank_out = 0;
+    return;
+  }
+  for (int e = tid; e < n * n; e += SJ_T) {
+    const int i = e % n, j = e / n;
+    B[i * ld + j] = 0.5 * (T.A[i + (long long)j * n] + T.A[j + (long long)i * n]);
+    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double f = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) f += B[i * ld + j] * B[i * ld + j];
+    s_fro = sqrt(f);
+  }
+  __syncthreads();
+  const double tol_abs = 2.220446049250313e-16 * s_fro;
+  const int nn = n + (n & 1), np = nn / 2;
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    for (int step = 0; step < nn - 1; ++step) {
+      // rotation parameters, one thread per pair
+      for (int pi = tid; pi < np; pi += SJ_T) {
+        int p = (step + pi) % (nn - 1);
+        int q = pi == 0 ? nn - 1 : (step - pi + nn - 1) % (nn - 1);
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, sn = 0.0;
+        if (q < n) {
+          const double bpq = B[p * ld + q];
+          if (fabs(bpq) > tol_abs) {
+            const double tau = (B[q * ld + q] - B[p * ld + p]) / (2.0 * bpq);
+            const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = rsqrt(1.0 + t * t);
+            sn = t * c;
+            s_rot = 1;
+          }
+        }
+        rc[pi] = c;
+        rs[pi] = sn;
+        rp[pi] = p;
+        rq[pi] = q < n ? q : -1;
+      }
+      __syncthreads();
+      // rows p, q of B
+      for (int e = tid; e < np * n; e += SJ_T) {
+        const int pi = e / n, k = e % n, q = rq[pi];
+        if (q < 0 || rs[pi] == 0.0) continue;
+        const int p = rp[pi];
+        const double c = rc[pi], sn = rs[pi];
+        const double x = B[p * ld + k], y = B[q * ld + k];
+        B[p * ld + k] = c * x - sn * y;
+        B[q * ld + k] = sn * x + c * y;
+      }
+      __syncthreads();
+      // columns p, q of B and of V
+      for (int e = tid; e < np * n; e += SJ_T) {
+        const int pi = e / n, k = e % n, q = rq[pi];
+        if (q < 0 || rs[pi] == 0.0) continue;
+        const int p = rp[pi];
+        const double c = rc[pi], sn = rs[pi];
+        const double x = B[k * ld + p], y = B[k * ld + q];
+        B[k * ld + p] = c * x - sn * y;
+        B[k * ld + q] = sn * x + c * y;
+        const double vx = V[k * ld + p], vy = V[k * ld + q];
+        V[k * ld + p] = c * vx - sn * vy;
+        V[k * ld + q] = sn * vx + c * vy;
+      }
+      __syncthreads();
+    }
+    if (!s_rot) break;
+    __syncthreads();
+  }
+  // eigenvalues, order by |lam| descending (ties by index), scaled output
+  __shared__ int cnt;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  for (int p = tid; p < n; p += SJ_T) {
+    const double lp = fabs(B[p * ld + p]);
+    int rk = 0;
+    for (int q = 0; q < n; ++q) {
+      const double lq = fabs(B[q * ld + q]);
+      rk += (lq > lp || (lq == lp && q < p)) ? 1 : 0;
+    }
+    if (lp > T.cut) atomicAdd(&cnt, 1);
+    T.sig[rk] = lp;
+    const double lam = B[p * ld + p];
+    for (int k = 0; k < n; ++k) {
+      T.A[k + (long long)rk * n] = V[k * ld + p] * lam;
+      T.V[k + (long long)rk * n] = V[k * ld + p];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *T.rank_out = cnt;
+}
+
+void sym_jacobi(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st) {
+  static size_t lim = enable_max_dyn_smem(sym_jacobi_kernel);
+  if (ntask <= 0) return;
+  size_t bytes = ((size_t)2 * max_n * (max_n + 1) + 4 * 96) * 8;
+  if (bytes > lim) throw CudaError("sym_jacobi: core too large for shared memory");
+  sym_jacobi_kernel<<<ntask, SJ_T, bytes, st>>>(d_tasks);
   TLRG_CUDA(cudaGetLastError());
 }
 
