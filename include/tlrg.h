@@ -67,6 +67,9 @@ typedef struct {
   double kt_gemm_seconds;    /* summed grouped-GEMM launch time (TLRG_KTIMING=1) */
   double kt_gemm_flops;      /* flops of those launches */
   int64_t kt_gemm_launches;
+  double t_ara_kernel;       /* CUDA-event time of the fused ARA kernels (dominant kernel) */
+  double flops_ara_kernel;   /* algorithmic FP64 flops they executed */
+  int64_t ara_kernel_launches;
 } tlrg_stats;
 
 typedef struct {

@@ -42,7 +42,9 @@ class StatsC(C.Structure):
                 ("t_compensation", C.c_double), ("flops_exec", C.c_double),
                 ("flops_gemm_ref", C.c_double), ("kernel_launches", C.c_int64),
                 ("t_device", C.c_double), ("kt_gemm_seconds", C.c_double),
-                ("kt_gemm_flops", C.c_double), ("kt_gemm_launches", C.c_int64)]
+                ("kt_gemm_flops", C.c_double), ("kt_gemm_launches", C.c_int64),
+                ("t_ara_kernel", C.c_double), ("flops_ara_kernel", C.c_double),
+                ("ara_kernel_launches", C.c_int64)]
 
 
 class StatusC(C.Structure):

@@ -190,6 +190,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   bool recomp_in_kernel = false;
   double *Uo = nullptr, *Vo = nullptr;
   int* rank_in = nullptr;
+  double* fl_dev = nullptr;
+  std::vector<double> h_fl(T, 0.0);
   std::vector<int> h_rank_in(T, -1);
   std::vector<std::pair<cudaGraphExec_t, cudaGraph_t>> graph_cleanup;
   if (use_fused) {
@@ -246,6 +248,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     fa.recompress = recomp_in_kernel ? 1 : 0;
     fa.cut = (1.0 - 1.0 / cfg.safety) * cfg.eps;
     fa.rank_out = rank_in;
+    fl_dev = C.buf<double>("fusedFlops", (size_t)T);
+    fa.flops_out = fl_dev;
     const char* fp = std::getenv("TLRG_FUSED_PROF");
     long long* dprof = nullptr;
     if (fp && fp[0] == '1') {
@@ -398,6 +402,9 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   if (recomp_in_kernel)
     TLRG_CUDA(cudaMemcpyAsync(h_rank_in.data(), rank_in, sizeof(int) * T, cudaMemcpyDeviceToHost,
                               C.st));
+  if (fl_dev)
+    TLRG_CUDA(cudaMemcpyAsync(h_fl.data(), fl_dev, sizeof(double) * T, cudaMemcpyDeviceToHost,
+                              C.st));
   C.wait();
   for (auto& gc : graph_cleanup) {
     cudaGraphExecDestroy(gc.first);
@@ -412,6 +419,12 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     C.launches += (long long)hact[1] * 16;
   }
   cst.t_sampling += tm.sec();  // the fused round loop (draws, sampling, orthog, absorb)
+  if (use_fused) {
+    cst.t_fused += tm.sec();
+    cst.fused_launches += 1;
+    for (int s = 0; s < T; ++s) cst.flops_fused += h_fl[s];
+    C.flops += 0.0;
+  }
   for (int s = 0; s < T; ++s) {
     q[s] = hq[s];
     h_av[s] = hav[s];

@@ -825,7 +825,14 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
       t_prev = t;
     }
   };
+  double fl = 0.0;  // algorithmic flops of this CTA (thread 0)
   while (!s_done && s_rounds < A.max_rounds) {
+    if (threadIdx.x == 0) {
+      const double r = rows, c = cols, kw = sl.Ad ? 0.0 : KW, b2 = bs;
+      fl += sl.Ad ? 2.0 * r * c * b2 : 2.0 * kw * (c + r) * b2;  // sampling
+      fl += 2.0 * r * b2 + 4.0 * 2.0 * r * b2 * b2;               // tau + panel MGS2 x 2 sweeps
+      fl += 2.0 * 2.0 * 2.0 * r * s_q * b2;                       // BGS deflation, 2 sweeps
+    }
     // ---- draw: make sure Omega and every possible replacement are available
     const double* Om;
     {
@@ -959,8 +966,16 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
     if (q == 0) rf = 0;
     else if (q <= 16) rf = recompress_tile<2>(A, sl, T, S, q, &s_flag);
     else if (q <= FUSED_QMAX) rf = recompress_tile<4>(A, sl, T, S, q, &s_flag);
-    if (threadIdx.x == 0) A.rank_out[s] = rf;
+    if (threadIdx.x == 0) {
+      A.rank_out[s] = rf;
+      if (rf >= 0 && q > 0) {
+        const double r = rows, c = cols, kw = sl.Ad ? 0.0 : KW, qq = q;
+        fl += sl.Ad ? 2.0 * r * c * qq : 2.0 * kw * (r + c) * qq;  // exit projection
+        fl += 4.0 * 2.0 * c * qq * qq + 2.0 * (r + c) * qq * rf;   // orthog of B + final products
+      }
+    }
   }
+  if (threadIdx.x == 0 && A.flops_out) A.flops_out[s] = fl;
   if (threadIdx.x == 0) *(volatile int*)&s_stop = 1;
   if (A.prof && threadIdx.x == 0) {
     pc[6] = clock64() - t_begin;

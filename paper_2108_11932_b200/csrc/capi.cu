@@ -494,6 +494,9 @@ int tlrg_factor_stats(tlrg_factor f, tlrg_stats* o, int32_t* ara_rounds, double*
     o->kt_gemm_seconds = S.kt_gemm_seconds;
     o->kt_gemm_flops = S.kt_gemm_flops;
     o->kt_gemm_launches = S.kt_gemm_launches;
+    o->t_ara_kernel = S.t_fused;
+    o->flops_ara_kernel = S.flops_fused;
+    o->ara_kernel_launches = S.fused_launches;
   }
   int nb = f->f->L->nb;
   if (ara_rounds)

@@ -203,6 +203,8 @@ struct ColumnStats {
   double t_sampling = 0, t_orthog = 0, t_projection = 0, t_recompress = 0, t_dense = 0;
   long long tile_rounds = 0;
   double flops_ref = 0;  // reference-formulation sampling+projection flops
+  double t_fused = 0, flops_fused = 0;  // fused ARA kernel: event time and in-kernel flops
+  long long fused_launches = 0;
 };
 
 // Column machinery shared by the factorization and the building-block API.
@@ -298,6 +300,8 @@ struct Stats {
   uint64_t tile_rounds_resident = 0;
   double t_recompress = 0, t_compensation = 0, flops_exec = 0, flops_ref = 0;
   double t_device = 0;        // CUDA-event time of the whole factorization
+  double t_fused = 0, flops_fused = 0;  // fused ARA kernel (the dominant kernel)
+  long long fused_launches = 0;
   double kt_gemm_seconds = 0, kt_gemm_flops = 0;  // per-launch GEMM timing (KTIMING)
   long long kt_gemm_launches = 0;
   long long launches = 0;

@@ -481,6 +481,9 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     S.t_projection += cst.t_projection;
     S.t_recompress += cst.t_recompress;
     S.flops_ref += cst.flops_ref;
+    S.t_fused += cst.t_fused;
+    S.flops_fused += cst.flops_fused;
+    S.fused_launches += cst.fused_launches;
     // ---- join: diagonal status (one small read) ---------------------------------
     TLRG_CUDA(cudaStreamWaitEvent(C.st, de3.e, 0));
     int* hs = C.pinned_ints(4);
@@ -581,7 +584,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   C.ktiming = false;
   TLRG_CUDA(cudaMemcpy(S.pivot_trace.data(), piv, sizeof(double) * nb, cudaMemcpyDeviceToHost));
   S.wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_wall0).count();
-  S.flops_exec = C.flops - flops0;
+  S.flops_exec = C.flops - flops0 + S.flops_fused;
   S.launches = C.launches - launches0;
   // dense-phase reference flops: sum_{j<k} (4m k_kj^2 + 2 m^2 k_kj)
   for (int k = 0; k < nb; ++k)

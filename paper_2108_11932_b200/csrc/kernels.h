@@ -196,6 +196,7 @@ struct FusedArgs {
   int recompress;      // run the exit projection + SVD recompression in-kernel
   double cut;          // (1 - 1/eta) eps
   int* rank_out;       // final rank, or -1 when the tile needs the batched fallback
+  double* flops_out;   // per slot: algorithmic FP64 flops executed by the CTA
 };
 constexpr int FUSED_QMAX = 32;  // widest basis recompressed in-kernel
 bool ara_fused_supported(int maxrows, int bs, int window);

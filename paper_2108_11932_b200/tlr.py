@@ -301,6 +301,9 @@ class FactorStats:
     kt_gemm_seconds: float = 0
     kt_gemm_flops: float = 0
     kt_gemm_launches: int = 0
+    t_ara_kernel: float = 0
+    flops_ara_kernel: float = 0
+    ara_kernel_launches: int = 0
     ara_rounds: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
     pivot_trace: np.ndarray = field(default_factory=lambda: np.zeros(0))
 
