@@ -85,6 +85,21 @@ void tlrg_default_factor_options(tlrg_factor_options* o);
 int tlrg_create(int device, tlrg_ctx* ctx, tlrg_status* st);
 void tlrg_destroy(tlrg_ctx ctx);
 
+/* ------------------------------------------------------------ multi-GPU --
+ * Intra-column split: with a communicator attached,
+ * tlrg_factorize deals every column's rank-sorted active tiles round-robin
+ * over the ranks (ARA + recompression + TRSM of its share on each GPU, diagonal
+ * path replicated) and replicates the new U/V panel with one variable-size
+ * all-gather per column.  The factor is bitwise identical for any rank count.
+ * NCCL transport: one process per GPU; rank 0 calls tlrg_comm_nccl_id and the
+ * 128-byte id is shared out of band.  Local transport: `world` contexts in one
+ * process, each factorization driven by its own host thread (tests). */
+int tlrg_comm_nccl_id(uint8_t* id /* 128 bytes */, tlrg_status* st);
+int tlrg_comm_attach_nccl(tlrg_ctx ctx, int32_t rank, int32_t world, const uint8_t* id,
+                          tlrg_status* st);
+int tlrg_comm_attach_local(tlrg_ctx* ctxs, int32_t world, tlrg_status* st);
+void tlrg_comm_detach(tlrg_ctx ctx);
+
 /* ------------------------------------------------------------------ store --
  * TlrMatrix(n, b) + payload upload (replaces tlr::TlrMatrix, tlr_matrix.hpp:26-59
  * and read_tlr's in-memory result).  ranks has nb(nb-1)/2 entries. */

@@ -62,6 +62,11 @@ SIGNATURES = {
     "tlrg_default_factor_options": (None, [C.POINTER(FactorOptionsC)]),
     "tlrg_create": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(StatusC)]),
     "tlrg_destroy": (None, [vp]),
+    "tlrg_comm_nccl_id": (C.c_int, [C.POINTER(C.c_uint8), C.POINTER(StatusC)]),
+    "tlrg_comm_attach_nccl": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8),
+                                        C.POINTER(StatusC)]),
+    "tlrg_comm_attach_local": (C.c_int, [C.POINTER(vp), C.c_int32, C.POINTER(StatusC)]),
+    "tlrg_comm_detach": (None, [vp]),
     "tlrg_matrix_upload": (C.c_int, [vp, C.c_int64, C.c_int32, C.c_double, dp, ip, dp, dp,
                                      C.POINTER(vp), C.POINTER(StatusC)]),
     "tlrg_matrix_info": (C.c_int, [vp, C.POINTER(C.c_int64), ip, ip, dp]),

@@ -561,8 +561,9 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     utot += (long long)S.rows[s] * fr[s];
     vtot += (long long)cols * fr[s];
   }
-  double* Up = utot ? store.alloc((size_t)utot) : nullptr;
-  double* Vp = vtot ? store.alloc((size_t)vtot) : nullptr;
+  // [U panel | V panel] in one allocation (one contiguous multi-GPU send buffer)
+  double* Up = (utot + vtot) ? store.alloc((size_t)(utot + vtot)) : nullptr;
+  double* Vp = vtot ? Up + utot : nullptr;
   std::vector<GemmProblem> pu;
   std::vector<CopyItem> cpy;
   long long uo = 0, vo = 0;

@@ -293,6 +293,23 @@ int tlrg_create(int device, tlrg_ctx* out, tlrg_status* st) {
 }
 void tlrg_destroy(tlrg_ctx c) { delete c; }
 
+int tlrg_comm_attach_nccl(tlrg_ctx ctx, int32_t rank, int32_t world, const uint8_t* id,
+                          tlrg_status* st) {
+  return guarded(st, [&] {
+    if (world < 1 || rank < 0 || rank >= world) config_error("tlrg_comm_attach_nccl: bad rank/world");
+    TLRG_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.comm = world > 1 ? make_nccl_comm(rank, world, id) : nullptr;
+  });
+}
+int tlrg_comm_attach_local(tlrg_ctx* ctxs, int32_t world, tlrg_status* st) {
+  return guarded(st, [&] {
+    if (world < 1) config_error("tlrg_comm_attach_local: bad world");
+    auto comms = make_local_comms(world);
+    for (int r = 0; r < world; ++r) ctxs[r]->c.comm = world > 1 ? comms[r] : nullptr;
+  });
+}
+void tlrg_comm_detach(tlrg_ctx ctx) { ctx->c.comm.reset(); }
+
 int tlrg_matrix_upload(tlrg_ctx ctx, int64_t n, int32_t b, double eps, const double* diag,
                        const int32_t* ranks, const double* U, const double* V, tlrg_matrix* out,
                        tlrg_status* st) {

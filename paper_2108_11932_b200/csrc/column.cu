@@ -197,7 +197,7 @@ void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPre
 
 std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
                                    const AraCfg& cfg, Store& store, ColumnStats& cst,
-                                   StreamPrep* pre) {
+                                   StreamPrep* pre, int part_rank, int part_world) {
   const int nb = M.nb, b = M.b, rk = M.rows(k), bs = cfg.bs, K = cs.K;
   std::vector<TileResult> res;
   for (int i = k + 1; i < nb; ++i) {
@@ -206,7 +206,15 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
     res.push_back(r);
   }
   if (res.empty()) return res;
-  const std::vector<int> queue = column_queue(M, k);
+  std::vector<int> queue = column_queue(M, k);
+  if (part_world > 1) {
+    // intra-column split: slot s of the rank-sorted queue
+    // belongs to rank s % world, which balances the fat near-diagonal tiles
+    std::vector<int> mine;
+    for (size_t s = 0; s < queue.size(); ++s)
+      if ((int)(s % part_world) == part_rank) mine.push_back(queue[s]);
+    queue.swap(mine);
+  }
   const int T = (int)queue.size();
   if (T == 0) return res;
 

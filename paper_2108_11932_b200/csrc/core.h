@@ -55,8 +55,21 @@ struct Store {
   ~Store();
 };
 
+struct Ctx;
+// Transport of the multi-GPU column exchange (comm.cu): NCCL or in-process ranks.
+struct Comm {
+  int rank = 0, world = 1;
+  virtual ~Comm() = default;
+  // host ints: every rank sends n, receives n * world (rank-major)
+  virtual void allgather_ints(Ctx& C, const int* send, int n, int* recv) = 0;
+  // device buffers: rank r's `counts[r]` doubles land in dst[r] on every other rank
+  virtual void broadcast_all(Ctx& C, const double* mine, const std::vector<double*>& dst,
+                             const std::vector<long long>& counts) = 0;
+};
+
 struct Ctx {
   int device = 0;
+  std::shared_ptr<Comm> comm;  // set for multi-GPU factorizations (world > 1)
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;  // side stream (gaussian stream pre-generation)
   cudaStream_t sd = nullptr;   // diagonal-path stream (SYRK, compensation, POTRF, L_kk^-1)
@@ -282,7 +295,13 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
 // allocated from `store` (U: sum rows(i)*r, V: rk x sum r contiguous).
 std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
                                    const AraCfg& cfg, Store& store, ColumnStats& cst,
-                                   StreamPrep* pre = nullptr);
+                                   StreamPrep* pre = nullptr, int part_rank = 0,
+                                   int part_world = 1);
+// multi-GPU: replicate the column's new U/V panel (comm.cu)
+void exchange_column(Ctx& C, Comm& cm, const Matrix& M, int k, const std::vector<int>& queue,
+                     std::vector<TileResult>& res, double* mine, Store& store);
+std::shared_ptr<Comm> make_nccl_comm(int rank, int world, const uint8_t* id);
+std::vector<std::shared_ptr<Comm>> make_local_comms(int world);
 // slot order of column k's ARA (rank-sorted, structural zeros removed) and the
 // early stream pre-generation for it (call at the start of the column)
 std::vector<int> column_queue(const Matrix& M, int k);

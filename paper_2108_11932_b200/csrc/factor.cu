@@ -475,7 +475,8 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     }
     // ---- ARA over the column (main stream) -------------------------------------
     ColumnStats cst;
-    std::vector<TileResult> res = column_ara(C, M, k, cs, cfg, *store, cst, &prep);
+    const int prank = C.comm ? C.comm->rank : 0, pworld = C.comm ? C.comm->world : 1;
+    std::vector<TileResult> res = column_ara(C, M, k, cs, cfg, *store, cst, &prep, prank, pworld);
     S.t_sampling += cst.t_sampling;
     S.t_orthog += cst.t_orthog;
     S.t_projection += cst.t_projection;
@@ -531,10 +532,14 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     // ---- TRSM of the new panel (one GEMM with the precomputed operator) --------
     cudaEventRecord(e4.e, C.st);
     double* Vp = nullptr;
+    double* Up0 = nullptr;
     long long ncols = 0;
     for (auto& r : res) {
-      if (r.rank > 0 && !Vp) Vp = r.V;
-      ncols += r.rank;
+      if (r.rank > 0 && !Vp) {
+        Vp = r.V;
+        Up0 = r.U;
+      }
+      ncols += r.rank;  // this rank's tiles only (the others are still empty)
       S.ara_rounds[k] += r.rounds;
     }
     S.tile_rounds_resident += S.ara_rounds[k];
@@ -550,6 +555,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       C.gemm(pr);
       ++C.launches;
     }
+    if (pworld > 1) exchange_column(C, *C.comm, M, k, column_queue(M, k), res, Up0, *store);
     for (auto& r : res) {
       long long t = M.t(r.i, k);
       M.rank[t] = r.rank;

@@ -134,6 +134,30 @@ class Context:
             cls._default = Context(0)
         return cls._default
 
+    # ---- multi-GPU (intra-column tile split) -------------------
+    def attach_nccl(self, rank: int, world: int, uid: bytes):
+        """Join an NCCL communicator (one process per GPU); `uid` comes from
+        nccl_unique_id() on rank 0, shared out of band."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        _call(self.lib.tlrg_comm_attach_nccl, self.h, rank, world, buf)
+
+    def detach(self):
+        self.lib.tlrg_comm_detach(self.h)
+
+
+def nccl_unique_id(ctx=None) -> bytes:
+    lib = ctx.lib if ctx is not None else L.load()
+    buf = (C.c_uint8 * 128)()
+    _call(lib.tlrg_comm_nccl_id, buf)
+    return bytes(buf)
+
+
+def attach_local(ctxs):
+    """In-process ranks: factorizations on these contexts, each driven by its
+    own host thread, split every column between them."""
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    _call(ctxs[0].lib.tlrg_comm_attach_local, arr, len(ctxs))
+
 
 def _ctx(ctx):
     return ctx if ctx is not None else Context.default()
