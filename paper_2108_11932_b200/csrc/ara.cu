@@ -250,6 +250,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     fa.rank_out = rank_in;
     fl_dev = C.buf<double>("fusedFlops", (size_t)T);
     fa.flops_out = fl_dev;
+    fa.mgs_passes = 2;  // MGS2 as the reference (one pass measurably changes ranks/rounds)
     const char* fp = std::getenv("TLRG_FUSED_PROF");
     long long* dprof = nullptr;
     if (fp && fp[0] == '1') {

@@ -273,6 +273,7 @@ struct TileCtx {
   long long* cur;  // smem cursor (absolute stream position)
   long long* av;   // smem count of values produced (producer warp)
   int wlim;        // panel columns actually present (<= BS)
+  int passes;      // Gram-Schmidt passes per column and sweep (reference: 2)
 };
 
 // Reduce-scatter of N (16 or 32) values over a warp: afterwards every lane
@@ -388,7 +389,7 @@ __device__ __forceinline__ void mgs_column(TileCtx& T, FSmem& S, double (&y)[RPT
   double* rpj = S.Rp + J * BS;
   if (J > 0) {
     cgs_pass_reg<BS, J>(y, S, rpj, par);
-    cgs_pass_reg<BS, J>(y, S, rpj, par);
+    if (T.passes > 1) cgs_pass_reg<BS, J>(y, S, rpj, par);
   }
   double nj = cta_norm<BS>(y, J, S, par);
   if (!(nj >= tau)) {
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
     stream_producer(A, s, &s_rel, &s_av, &s_stop, prod);
     return;
   }
-  TileCtx T{&sl, A.G, s, rows, cols, bs, ldy, 0, &s_cur, &s_av, bs};
+  TileCtx T{&sl, A.G, s, rows, cols, bs, ldy, 0, &s_cur, &s_av, bs, A.mgs_passes};
   const double* gb = A.G.buf + (long long)s * A.G.cap;
   const int kA = sl.kA, K = A.K, KW = kA + K;
   const int ldw = (KW + 1) & ~1;

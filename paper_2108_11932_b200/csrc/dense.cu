@@ -28,7 +28,6 @@ namespace tlrg {
 //            tile A_rc -= L_rp L_cp^T spread over all CTAs;               grid.sync
 constexpr int PB = 32;
 constexpr int PO_T = 256;
-constexpr int PO_W = PO_T / 32;
 
 // unblocked Cholesky of the pw x pw block (pw <= 32) held one row per lane;
 // returns the failing column or -1.  v[j] = L(lane, j) on exit (j <= lane).
