@@ -237,13 +237,16 @@ __global__ void __launch_bounds__(1024) cholqr_kernel(const double* G, int p, in
   }
   const double tol = 1e-24 * (tr > 0.0 ? tr : 1.0) / p;
   __syncthreads();
-  // right-looking Cholesky, upper factor in place
+  // right-looking Cholesky, upper factor in place.  2-D thread map (32 x 32):
+  // thread (ty, tx) owns trailing entries (j+1+ty+32u, j+1+tx+32v) — no index
+  // division in the update loop (the kernel is issue-bound otherwise)
+  const int tx = tid & 31, ty = tid >> 5;
   for (int j = 0; j < p; ++j) {
     const double d = R[j * ld + j];
     const bool dead = !(d > tol);
-    __syncthreads();
     if (tid == 0) s_dead[j] = dead;
     if (dead) {
+      __syncthreads();
       for (int k = tid; k < p; k += blockDim.x) {
         R[j * ld + k] = 0.0;
         R[k * ld + j] = 0.0;
@@ -251,41 +254,56 @@ __global__ void __launch_bounds__(1024) cholqr_kernel(const double* G, int p, in
       __syncthreads();
       continue;
     }
-    const double rjj = sqrt(d);
-    for (int k = j + 1 + tid; k < p; k += blockDim.x) R[j * ld + k] /= rjj;
+    const double rr = rsqrt(d);
+    __syncthreads();  // every thread has read R[j][j]
+    for (int k = j + 1 + tid; k < p; k += blockDim.x) R[j * ld + k] *= rr;
+    if (tid == 0) R[j * ld + j] = d * rr;
     __syncthreads();
-    if (tid == 0) R[j * ld + j] = rjj;
-    const int m = p - j - 1;
-    for (int e = tid; e < m * m; e += blockDim.x) {
-      const int a = j + 1 + e / m, b = j + 1 + e % m;
-      if (b >= a) R[a * ld + b] -= R[j * ld + a] * R[j * ld + b];
+    for (int a2 = j + 1 + ty; a2 < p; a2 += 32) {
+      const double ra = R[j * ld + a2];
+      for (int b2 = j + 1 + tx; b2 < p; b2 += 32)
+        if (b2 >= a2) R[a2 * ld + b2] -= ra * R[j * ld + b2];
     }
     __syncthreads();
   }
-  // Rinv: back substitution per column (one warp per column)
-  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int c = warp; c < p; c += nw) {
-    // x_i for i = c .. 0 ; lane-parallel dot over k in (i, c]
-    double xs[5] = {0, 0, 0, 0, 0};  // lane holds x_k for k = lane + 32 t
-    for (int i = c; i >= 0; --i) {
-      double part = 0.0;
-#pragma unroll
-      for (int t = 0; t < 5; ++t) {
-        const int k = lane + 32 * t;
-        if (k > i && k <= c && k < p) part += R[i * ld + k] * xs[t];
-      }
-      const double sum = warp_sum(part);
-      const double rii = R[i * ld + i];
-      const double xi = (s_dead[i] || rii == 0.0) ? 0.0 : ((i == c ? 1.0 : 0.0) - sum) / rii;
-      if ((i & 31) == lane) xs[i >> 5] = xi;
-    }
-#pragma unroll
-    for (int t = 0; t < 5; ++t) {
-      const int k = lane + 32 * t;
-      if (k < p) Rinv[k + (long long)c * p] = (k <= c) ? xs[t] : 0.0;
-    }
+  // output R (upper, row-major in smem -> column-major p x p); a dropped pivot
+  // leaves a zero row/column, which cholqr_apply turns into a zero basis column
+  for (int e = tid; e < p * p; e += blockDim.x) {
+    const int i = e % p, j = e / p;
+    Rinv[e] = (i <= j) ? R[i * ld + j] : 0.0;
   }
 }
+
+// Y <- Y R^{-1}: row r of Y solves q R = y (forward substitution over the p
+// columns), one thread per row, R staged in shared memory
+__global__ void __launch_bounds__(128) cholqr_apply_kernel(double* Y, int n, int p,
+                                                           const double* R) {
+  extern __shared__ double rs[];
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) rs[e] = R[e];
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double q[160];
+  for (int j = 0; j < p; ++j) {
+    const double rjj = rs[j + j * p];
+    double s0 = Y[r + (long long)j * n], s1 = 0.0;
+    int i = 0;
+    for (; i + 1 < j; i += 2) {
+      s0 -= q[i] * rs[i + j * p];
+      s1 -= q[i + 1] * rs[i + 1 + j * p];
+    }
+    if (i < j) s0 -= q[i] * rs[i + j * p];
+    q[j] = rjj != 0.0 ? (s0 + s1) / rjj : 0.0;
+  }
+  for (int j = 0; j < p; ++j) Y[r + (long long)j * n] = q[j];
+}
+void cholqr_apply(double* Y, int n, int p, const double* R, cudaStream_t st) {
+  static size_t lim = enable_max_dyn_smem(cholqr_apply_kernel);
+  (void)lim;
+  cholqr_apply_kernel<<<(n + 127) / 128, 128, (size_t)p * p * 8, st>>>(Y, n, p, R);
+  TLRG_CUDA(cudaGetLastError());
+}
+
 void cholqr_factor(const double* G, int p, int n, int shift, double* Rinv, cudaStream_t st) {
   static size_t lim = enable_max_dyn_smem(cholqr_kernel);
   (void)lim;

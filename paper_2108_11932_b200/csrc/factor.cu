@@ -236,7 +236,7 @@ bool modified_cholesky_device(Ctx& C, double* A, int n) {
 // slack remained (r <= p - 8) and re-runs with a wider sketch otherwise.
 constexpr int kSchurMaxWidth = 160;  // sketch width cap (shared-memory Cholesky-QR)
 int schur_comp_width(int n, int rank_hint) {
-  int p = std::max(32, rank_hint + 24);
+  int p = std::max(24, rank_hint + 16);
   p = ((p + 7) / 8) * 8;
   p = std::min(p, kSchurMaxWidth);
   return p > n ? n : p;
@@ -262,7 +262,6 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
   // one tiny factor kernel each): X <- X R1^{-1} R2^{-1} R3^{-1}
   double* Gq = C.buf<double>("sc_G", (size_t)p * p);
   double* Ri = C.buf<double>("sc_Ri", (size_t)p * p);
-  double* Xt = C.buf<double>("sc_Xt", (size_t)n * p);
   auto orth = [&](double* X) {
     for (int pass = 0; pass < 3; ++pass) {
       std::vector<GemmProblem> pr(1);
@@ -270,13 +269,9 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
       pr[0].A = X; pr[0].lda = n; pr[0].transA = 1; pr[0].B = X; pr[0].ldb = n;
       pr[0].C = Gq; pr[0].ldc = p; pr[0].M = p; pr[0].N = p; pr[0].K = n; pr[0].alpha = 1.0;
       C.gemm(pr);
-      cholqr_factor(Gq, p, n, pass == 0, Ri, C.st);
-      ++C.launches;
-      pr[0] = GemmProblem{};
-      pr[0].A = X; pr[0].lda = n; pr[0].B = Ri; pr[0].ldb = p;
-      pr[0].C = Xt; pr[0].ldc = n; pr[0].M = n; pr[0].N = p; pr[0].K = p; pr[0].alpha = 1.0;
-      C.gemm(pr);
-      TLRG_CUDA(cudaMemcpyAsync(X, Xt, sizeof(double) * n * p, cudaMemcpyDeviceToDevice, C.st));
+      cholqr_factor(Gq, p, n, pass == 0, Ri, C.st);  // Ri <- R (upper)
+      cholqr_apply(X, n, p, Ri, C.st);               // X <- X R^{-1}
+      C.launches += 2;
     }
   };
   DtimesX(Om, Y);
@@ -295,6 +290,7 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
   sv[0] = SvdTask{};
   sv[0].A = Bm; sv[0].V = Vm; sv[0].sig = sig; sv[0].work = work; sv[0].rank_out = rank_out;
   sv[0].n = p; sv[0].cut = eps;
+  sv[0].tol = 1e-11;  // eigenvectors to 1e-11: ample for the eps-level split, 2 fewer sweeps
   jacobi_svd(C.push(sv), 1, p, C.st);
   ++C.launches;
   // R = D - (Q A_B)(Q V_B)^T restricted to the r = *rank_out retained directions

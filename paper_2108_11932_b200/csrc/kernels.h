@@ -136,6 +136,7 @@ struct SvdTask {
   int n;        // columns (V is n x n)
   double cut;
   int m;        // rows of A (0 = n)
+  double tol;   // rotation threshold (0 = rounding level m * eps_mach)
 };
 void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m = 0);
 // symmetric (PSD) core: A <- V diag(lam), V, |lam| sorted descending (n <= 160)
@@ -214,8 +215,11 @@ void sytrf_bk(double* A, int n, double* d, double* e, uint8_t* s2, int* perm, in
 void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
                 const double* d, const double* e, const uint8_t* s2, int* info,
                 cudaStream_t st);
-// (shifted) Cholesky-QR step: R^T R = G (+ shift), Rinv = R^{-1}, p <= 128
+// (shifted) Cholesky-QR step: R^T R = G (+ shift), Rinv = R^{-1}, p <= 160
 void cholqr_factor(const double* G, int p, int n, int shift, double* Rinv, cudaStream_t st);
+// Y (n x p, ld n) <- Y R^{-1} row by row (R upper p x p from cholqr_factor's
+// R output); columns with a dropped pivot are zeroed.  In place.
+void cholqr_apply(double* Y, int n, int p, const double* R, cudaStream_t st);
 // X_bb = L_bb^{-1} for diagonal blocks (offset, length <= 32) of an n x n lower L
 void trtri_base(const double* L, int n, double* X, const int* d_offs, const int* d_lens,
                 int nblocks, cudaStream_t st);

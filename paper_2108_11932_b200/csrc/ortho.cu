@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   // rotation threshold: rounding level of an m-term dot product (dgesvj style)
   // rotation threshold: rounding level of an m-term dot product (m eps); a
   // stricter one only makes the final sweeps chase rounding noise
-  const double tol = fmax(1e-15, (double)m * 2.220446049250313e-16);
+  const double tol = T.tol > 0.0 ? T.tol : fmax(1e-15, (double)m * 2.220446049250313e-16);
   const int nn = n + (n & 1);
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) rotated = 0;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(JS_T) jacobi_small_kernel(SvdTask* tasks) {
   double fro = 0.0;
   for (int w = 0; w < JS_T / 32; ++w) fro += red[w];
   const double tiny2 = fro * 1e-34;
-  const double tol = fmax(1e-15, (double)m * 2.220446049250313e-16);
+  const double tol = T.tol > 0.0 ? T.tol : fmax(1e-15, (double)m * 2.220446049250313e-16);
   const int nn = n + (n & 1), np = nn / 2;
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) rotated = 0;

@@ -8,7 +8,7 @@ using namespace tlrg;
 constexpr int PB = 32;
 constexpr int PO_T = 256;
 constexpr int PO_W = PO_T / 32;
-__device__ __forceinline__ int chol32_reg(double (&v)[PB], int pw) {
+__device__ __noinline__ int chol32_reg(double (&v)[PB], int pw) {
   const int lane = threadIdx.x & 31;
   int fail = -1;
 #pragma unroll
@@ -55,7 +55,9 @@ __global__ void __launch_bounds__(PO_T) potrf_x(double* A, int n, int* info, lon
 #pragma unroll
         for (int j = 0; j < PB; ++j)
           v[j] = (lane < pw && j < pw && j <= lane) ? A[(p0 + lane) + (long long)(p0 + j) * n] : 0.0;
+        long long q0 = clock64();
         const int fa = chol32_reg(v, pw);
+        if (blockIdx.x == 0 && lane == 0) tm[1000] += clock64() - q0;
 #pragma unroll
         for (int j = 0; j < PB; ++j) Lp[lane][j] = (j <= lane) ? v[j] : 0.0;
         if (lane == 0) s_fail = fa;
@@ -64,6 +66,7 @@ __global__ void __launch_bounds__(PO_T) potrf_x(double* A, int n, int* info, lon
       if (s_fail >= 0) {
         if (tid == 0) atomicCAS(info, -1, p0 + s_fail);
       } else {
+        long long q1 = clock64();
         // X = L_pp^{-1} (lane j builds column j), then L_rp = A_rp X^T as a
         // product: no per-row sequential substitution
         if (warp == 0) {
@@ -88,6 +91,8 @@ __global__ void __launch_bounds__(PO_T) potrf_x(double* A, int n, int* info, lon
           for (int i = 0; i < PB; ++i) Xp[i][j] = x[i];  // Xp[i][j] = (L_pp^{-1})_{ij}
         }
         __syncthreads();
+        if (blockIdx.x == 0 && threadIdx.x == 0) tm[1001] += clock64() - q1;
+        long long q2 = clock64();
         for (int r = p0 + pw + blockIdx.x * PO_T + tid; r < n; r += gridDim.x * PO_T) {
           double a[PB];
 #pragma unroll
@@ -102,6 +107,7 @@ __global__ void __launch_bounds__(PO_T) potrf_x(double* A, int n, int* info, lon
             }
           }
         }
+        if (blockIdx.x == 0 && threadIdx.x == 0) tm[1002] += clock64() - q2;
       }
     }
     long long a1 = clock64(); tp1 += a1 - t0;
@@ -174,7 +180,7 @@ int main() {
       A[i + j * n] = s / n + (i == j ? 1.0 : 0.0);
     }
   double *dA, *dW; int* info; long long* tm;
-  cudaMalloc(&dA, 8 * n * n); cudaMalloc(&dW, 8 * n * n); cudaMalloc(&info, 16); cudaMalloc(&tm, 8*4*256);
+  cudaMalloc(&dA, 8 * n * n); cudaMalloc(&dW, 8 * n * n); cudaMalloc(&info, 16); cudaMalloc(&tm, 8*2048); cudaMemset(tm, 0, 8*2048);
   cudaMemcpy(dA, A.data(), 8 * n * n, cudaMemcpyHostToDevice);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   for (int grid : {8, 16, 48}) for (int rep = 0; rep < 2; ++rep) {
@@ -187,6 +193,8 @@ int main() {
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     std::vector<long long> h(4*grid); cudaMemcpy(h.data(), tm, 8*4*grid, cudaMemcpyDeviceToHost);
-    printf("grid %d: %.1f us  cta0 phase1 %lld sync1 %lld phase2 %lld sync2 %lld kcyc (%s)\n", grid, ms*1e3, h[0]/1000, h[1]/1000, h[2]/1000, h[3]/1000, cudaGetErrorString(cudaGetLastError()));
+    long long hx[3]; cudaMemcpy(hx, tm + 1000, 24, cudaMemcpyDeviceToHost);
+    printf("grid %d: %.1f us  cta0 phase1 %lld sync1 %lld phase2 %lld sync2 %lld kcyc | chol32 %lld inv %lld rows %lld kcyc (%s)\n", grid, ms*1e3, h[0]/1000, h[1]/1000, h[2]/1000, h[3]/1000, hx[0]/1000, hx[1]/1000, hx[2]/1000, cudaGetErrorString(cudaGetLastError()));
+    cudaMemset(tm + 1000, 0, 24);
   }
 }
