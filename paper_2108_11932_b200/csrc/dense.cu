@@ -86,43 +86,28 @@ __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int*
       if (s_fail >= 0) {
         if (tid == 0) atomicCAS(info, -1, p0 + s_fail);
       } else {
-        // X = L_pp^{-1} (lane j builds column j), then L_rp = A_rp X^T as a
-        // product: no per-row sequential substitution
-        if (warp == 0) {
-          double x[PB];
-#pragma unroll
-          for (int i = 0; i < PB; ++i) x[i] = 0.0;
-          const int j = lane;
-          if (j < pw) {
-            x[j] = 1.0 / Lp[j][j];
-#pragma unroll
-            for (int i = 1; i < PB; ++i) {
-              if (i > j && i < pw) {
-                double acc = 0.0;
-#pragma unroll
-                for (int k = 0; k < PB; ++k)
-                  if (k >= j && k < i) acc += Lp[i][k] * x[k];
-                x[i] = -acc / Lp[i][i];
-              }
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < PB; ++i) Xp[i][j] = x[i];  // Xp[i][j] = (L_pp^{-1})_{ij}
-        }
+        // L_rp = A_rp L_pp^{-T}: one thread per row, forward substitution in
+        // registers against L_pp in shared memory, reciprocal pivots precomputed
+        if (tid < pw) Xp[0][tid] = 1.0 / Lp[tid][tid];
         __syncthreads();
         for (int r = p0 + pw + blockIdx.x * PO_T + tid; r < n; r += gridDim.x * PO_T) {
-          double a[PB];
+          double x[PB];
 #pragma unroll
-          for (int t = 0; t < PB; ++t) a[t] = t < pw ? A[r + (long long)(p0 + t) * n] : 0.0;
+          for (int t = 0; t < PB; ++t) x[t] = t < pw ? A[r + (long long)(p0 + t) * n] : 0.0;
 #pragma unroll
-          for (int jj = 0; jj < PB; ++jj) {
-            if (jj < pw) {
-              double acc = 0.0;
+          for (int j = 0; j < PB; ++j) {
+            double s0 = x[j], s1 = 0.0;
 #pragma unroll
-              for (int t = 0; t <= jj; ++t) acc += a[t] * Xp[jj][t];
-              A[r + (long long)(p0 + jj) * n] = acc;
+            for (int t = 0; t + 1 < j; t += 2) {
+              s0 -= x[t] * Lp[j][t];
+              s1 -= x[t + 1] * Lp[j][t + 1];
             }
+            if (j & 1) s0 -= x[j - 1] * Lp[j][j - 1];
+            x[j] = j < pw ? (s0 + s1) * Xp[0][j] : 0.0;
           }
+#pragma unroll
+          for (int t = 0; t < PB; ++t)
+            if (t < pw) A[r + (long long)(p0 + t) * n] = x[t];
         }
       }
     }
@@ -138,7 +123,7 @@ __global__ void __launch_bounds__(PO_T) potrf_coop_kernel(double* A, int n, int*
     const int ntr = nt - p - 1;
     const int ntiles = ntr * (ntr + 1) / 2;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      int rr = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      int rr = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
       while (rr * (rr + 1) / 2 > t) --rr;
       while ((rr + 1) * (rr + 2) / 2 <= t) ++rr;
       const int cc = t - rr * (rr + 1) / 2;

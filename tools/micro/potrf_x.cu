@@ -8,7 +8,7 @@ using namespace tlrg;
 constexpr int PB = 32;
 constexpr int PO_T = 256;
 constexpr int PO_W = PO_T / 32;
-__device__ __noinline__ int chol32_reg(double (&v)[PB], int pw) {
+__device__ __forceinline__ int chol32_reg(double (&v)[PB], int pw) {
   const int lane = threadIdx.x & 31;
   int fail = -1;
 #pragma unroll
@@ -55,9 +55,7 @@ __global__ void __launch_bounds__(PO_T) potrf_x(double* A, int n, int* info, lon
 #pragma unroll
         for (int j = 0; j < PB; ++j)
           v[j] = (lane < pw && j < pw && j <= lane) ? A[(p0 + lane) + (long long)(p0 + j) * n] : 0.0;
-        long long q0 = clock64();
         const int fa = chol32_reg(v, pw);
-        if (blockIdx.x == 0 && lane == 0) tm[1000] += clock64() - q0;
 #pragma unroll
         for (int j = 0; j < PB; ++j) Lp[lane][j] = (j <= lane) ? v[j] : 0.0;
         if (lane == 0) s_fail = fa;
@@ -66,48 +64,29 @@ __global__ void __launch_bounds__(PO_T) potrf_x(double* A, int n, int* info, lon
       if (s_fail >= 0) {
         if (tid == 0) atomicCAS(info, -1, p0 + s_fail);
       } else {
-        long long q1 = clock64();
-        // X = L_pp^{-1} (lane j builds column j), then L_rp = A_rp X^T as a
-        // product: no per-row sequential substitution
-        if (warp == 0) {
+        // L_rp = A_rp L_pp^{-T}: one thread per row, forward substitution in
+        // registers against L_pp in shared memory, reciprocal pivots precomputed
+        if (tid < pw) Xp[0][tid] = 1.0 / Lp[tid][tid];
+        __syncthreads();
+        for (int r = p0 + pw + blockIdx.x * PO_T + tid; r < n; r += gridDim.x * PO_T) {
           double x[PB];
 #pragma unroll
-          for (int i = 0; i < PB; ++i) x[i] = 0.0;
-          const int j = lane;
-          if (j < pw) {
-            x[j] = 1.0 / Lp[j][j];
+          for (int t = 0; t < PB; ++t) x[t] = t < pw ? A[r + (long long)(p0 + t) * n] : 0.0;
 #pragma unroll
-            for (int i = 1; i < PB; ++i) {
-              if (i > j && i < pw) {
-                double acc = 0.0;
+          for (int j = 0; j < PB; ++j) {
+            double s0 = x[j], s1 = 0.0;
 #pragma unroll
-                for (int k = 0; k < PB; ++k)
-                  if (k >= j && k < i) acc += Lp[i][k] * x[k];
-                x[i] = -acc / Lp[i][i];
-              }
+            for (int t = 0; t + 1 < j; t += 2) {
+              s0 -= x[t] * Lp[j][t];
+              s1 -= x[t + 1] * Lp[j][t + 1];
             }
+            if (j & 1) s0 -= x[j - 1] * Lp[j][j - 1];
+            x[j] = j < pw ? (s0 + s1) * Xp[0][j] : 0.0;
           }
 #pragma unroll
-          for (int i = 0; i < PB; ++i) Xp[i][j] = x[i];  // Xp[i][j] = (L_pp^{-1})_{ij}
+          for (int t = 0; t < PB; ++t)
+            if (t < pw) A[r + (long long)(p0 + t) * n] = x[t];
         }
-        __syncthreads();
-        if (blockIdx.x == 0 && threadIdx.x == 0) tm[1001] += clock64() - q1;
-        long long q2 = clock64();
-        for (int r = p0 + pw + blockIdx.x * PO_T + tid; r < n; r += gridDim.x * PO_T) {
-          double a[PB];
-#pragma unroll
-          for (int t = 0; t < PB; ++t) a[t] = t < pw ? A[r + (long long)(p0 + t) * n] : 0.0;
-#pragma unroll
-          for (int jj = 0; jj < PB; ++jj) {
-            if (jj < pw) {
-              double acc = 0.0;
-#pragma unroll
-              for (int t = 0; t <= jj; ++t) acc += a[t] * Xp[jj][t];
-              A[r + (long long)(p0 + jj) * n] = acc;
-            }
-          }
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) tm[1002] += clock64() - q2;
       }
     }
     long long a1 = clock64(); tp1 += a1 - t0;
@@ -124,7 +103,7 @@ __global__ void __launch_bounds__(PO_T) potrf_x(double* A, int n, int* info, lon
     const int ntr = nt - p - 1;
     const int ntiles = ntr * (ntr + 1) / 2;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      int rr = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      int rr = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
       while (rr * (rr + 1) / 2 > t) --rr;
       while ((rr + 1) * (rr + 2) / 2 <= t) ++rr;
       const int cc = t - rr * (rr + 1) / 2;
@@ -193,8 +172,6 @@ int main() {
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     std::vector<long long> h(4*grid); cudaMemcpy(h.data(), tm, 8*4*grid, cudaMemcpyDeviceToHost);
-    long long hx[3]; cudaMemcpy(hx, tm + 1000, 24, cudaMemcpyDeviceToHost);
-    printf("grid %d: %.1f us  cta0 phase1 %lld sync1 %lld phase2 %lld sync2 %lld kcyc | chol32 %lld inv %lld rows %lld kcyc (%s)\n", grid, ms*1e3, h[0]/1000, h[1]/1000, h[2]/1000, h[3]/1000, hx[0]/1000, hx[1]/1000, hx[2]/1000, cudaGetErrorString(cudaGetLastError()));
-    cudaMemset(tm + 1000, 0, 24);
+    printf("grid %d: %.1f us  cta0 phase1 %lld sync1 %lld phase2 %lld sync2 %lld kcyc (%s)\n", grid, ms*1e3, h[0]/1000, h[1]/1000, h[2]/1000, h[3]/1000, cudaGetErrorString(cudaGetLastError()));
   }
 }
