@@ -15,6 +15,7 @@
 //           convergence / done.
 // Dense mode (build_tlr's DenseSampler, ara.hpp:43-57): Y = A_tile Omega.
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "stream.cuh"
@@ -301,6 +302,161 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[N]) {
   return r;
 }
 
+// ---- TMA-staged streaming of the big operand (sampling products) ----------
+// The A operands of the two sampling products ([V^A | U_k,:] and [U^A | H_i],
+// 4 KB columns) stream through shared memory by bulk copies (cp.async.bulk,
+// mbarrier completion, two stages of SCOL columns, padded stride so the
+// 16-byte fragment loads are bank-conflict free); compute on one stage
+// overlaps the copy of the next.
+constexpr int SCOL = 8;
+constexpr int SPAD = 520;
+struct Stager {
+  double* buf;    // 2 x SCOL x SPAD
+  uint64_t* bar;  // 2 mbarriers
+};
+template <class ACol>
+__device__ __forceinline__ void stage_issue(const Stager& st, int s, int c, int ncol, int len,
+                                            ACol acol) {
+  if (threadIdx.x == 0) {
+    const int c0 = c * SCOL, nc = min(SCOL, ncol - c0);
+    mbar_arrive_expect_tx(&st.bar[s], (unsigned)(nc * len * 8));
+    for (int j = 0; j < nc; ++j)
+      bulk_g2s(st.buf + (s * SCOL + j) * SPAD, acol(c0 + j), (unsigned)(len * 8), &st.bar[s]);
+  }
+}
+
+// out(m, n, v) for m < M: v = sgn(m) * sum_{k<Kd} acol(m)[k] * bcol(n)[k]; the M
+// columns are staged 8 at a time, the warps split k, partials reduced in a
+// fixed order.  Kd even, <= 8 * 64 * FW.
+template <int NT, class ACol, class BCol, class Sgn, class Out>
+__device__ void tn16_tma(int M, int Kd, ACol acol, BCol bcol, Sgn sgn, Out out, double* part,
+                         const Stager& st, unsigned& ph) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int nch = (M + SCOL - 1) / SCOL;
+  if (nch == 0 || Kd <= 0) return;
+  const int k8 = (Kd + 7) / 8, per = (k8 + FW - 1) / FW;
+  const int kb0 = warp * per, kb1 = min(k8, kb0 + per);
+  const double* bp[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) bp[j] = bcol(j * 8 + g);
+  stage_issue(st, 0, 0, M, Kd, acol);
+  if (nch > 1) stage_issue(st, 1, 1, M, Kd, acol);
+  for (int c = 0; c < nch; ++c) {
+    const int s = c & 1;
+    mbar_wait(&st.bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    const bool mv = c * SCOL + g < M;
+    const double* ap = st.buf + (s * SCOL + g) * SPAD;
+    double acc[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+    for (int kb = kb0; kb < kb1; ++kb) {
+      const int kk = kb * 8 + 2 * t;
+      const bool kv = kk < Kd;
+      const double2 a = (mv && kv) ? ld2(ap + kk) : make_double2(0.0, 0.0);
+      double2 b[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = kv ? ld2(bp[j] + kk) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        dmma_8x8x4(acc[j][0], acc[j][1], a.x, b[j].x);
+        dmma_8x8x4(acc[j][0], acc[j][1], a.y, b[j].y);
+      }
+    }
+    double* P = part + warp * 64 * NT;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      P[g * 8 * NT + j * 8 + 2 * t] = acc[j][0];
+      P[g * 8 * NT + j * 8 + 2 * t + 1] = acc[j][1];
+    }
+    cbar();
+    for (int e = threadIdx.x; e < 64 * NT; e += FT) {
+      const int m = c * SCOL + e / (8 * NT), n = e % (8 * NT);
+      if (m < M) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < FW; ++w) sum += part[w * 64 * NT + e];
+        out(m, n, sgn(m) * sum);
+      }
+    }
+    cbar();
+    if (c + 2 < nch) stage_issue(st, s, c + 2, M, Kd, acol);
+  }
+}
+
+// epi(r, c, v): v = sum_{k<Kd} acol(k)[r] * B[k + c*ldb]; the Kd columns of the
+// big operand are staged 8 at a time (one 8-k block per stage).
+template <int NT, class ACol, class Epi>
+__device__ void nn16_tma(int rows, int Kd, ACol acol, const double* B, int ldb, Epi epi,
+                         const Stager& st, unsigned& ph) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  constexpr int GPW = MAXROWS / 16 / FW;
+  const int ngr = (rows + 15) / 16;
+  const int nch = (Kd + SCOL - 1) / SCOL;
+  double acc[GPW][NT][2][2];
+#pragma unroll
+  for (int i = 0; i < GPW; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+      acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+  if (nch > 0) stage_issue(st, 0, 0, Kd, rows, acol);
+  if (nch > 1) stage_issue(st, 1, 1, Kd, rows, acol);
+  for (int c = 0; c < nch; ++c) {
+    const int s = c & 1;
+    const int kk = c * SCOL + 2 * t;
+    double2 aw[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const double* bj = B + kk + (long long)(j * 8 + g) * ldb;
+      aw[j] = kk + 1 < Kd ? ld2(bj) : make_double2(kk < Kd ? bj[0] : 0.0, 0.0);
+    }
+    mbar_wait(&st.bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    const double* c0p = st.buf + (s * SCOL + 2 * t) * SPAD;
+    const double* c1p = c0p + SPAD;
+    const bool v0 = kk < Kd, v1 = kk + 1 < Kd;
+#pragma unroll
+    for (int i = 0; i < GPW; ++i) {
+      const int gr = warp + FW * i;
+      const int r = gr * 16 + 2 * g;
+      double2 b0 = make_double2(0.0, 0.0), b1 = make_double2(0.0, 0.0);
+      if (gr < ngr && r < rows) {
+        if (v0) b0 = ld2(c0p + r);
+        if (v1) b1 = ld2(c1p + r);
+      }
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], aw[j].x, b0.x);
+        dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], aw[j].x, b0.y);
+        dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], aw[j].y, b1.x);
+        dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], aw[j].y, b1.y);
+      }
+    }
+    cbar();
+    if (c + 2 < nch) stage_issue(st, s, c + 2, Kd, rows, acol);
+  }
+#pragma unroll
+  for (int i = 0; i < GPW; ++i) {
+    const int gr = warp + FW * i;
+    if (gr >= ngr) continue;
+    const int r0 = gr * 16 + 4 * t;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int cc = j * 8 + g;
+      if (r0 < rows) {
+        epi(r0, cc, acc[i][j][0][0]);
+        epi(r0 + 1, cc, acc[i][j][1][0]);
+      }
+      if (r0 + 2 < rows) {
+        epi(r0 + 2, cc, acc[i][j][0][1]);
+        epi(r0 + 3, cc, acc[i][j][1][1]);
+      }
+    }
+  }
+  cbar();
+}
+
 // one classical pass of column j of the register-resident panel against the
 // columns p < j (each thread owns RPT tile rows).  Every warp writes its
 // reduce-scattered partial dots to shared memory (double-buffered by pass
@@ -521,7 +677,7 @@ __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
 // dense_kernels.cpp:422-454): A (n x n, ld n) <- U Sigma, V <- right vectors
 // (both unsorted); sig[] the column norms; perm[] orders them descending (ties
 // by index, like the batched kernel); returns #{sigma > cut}.
-__device__ int cta_jacobi_svd(double* A, double* V, double* sig, int* perm, int n, double cut,
+__device__ __noinline__ int cta_jacobi_svd(double* A, double* V, double* sig, int* perm, int n, double cut,
                               double* wred, int* flag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int e = threadIdx.x; e < n * n; e += FT) V[e] = (e % n == e / n) ? 1.0 : 0.0;
@@ -687,7 +843,7 @@ __device__ void stream_producer(const FusedArgs& A, int s, volatile long long* s
 //   B = E^T Q (cols x q) -> Z R = orthog(empty, B) (same panel MGS2, same stream)
 //   -> SVD of R cut at (1 - 1/eta) eps -> Uo = Q V_s, Vo = Z U_s sigma.
 template <int NTQ>
-__device__ int recompress_tile(const FusedArgs& A, const FusedSlot& sl, TileCtx& T, FSmem& S,
+__device__ __noinline__ int recompress_tile(const FusedArgs& A, const FusedSlot& sl, TileCtx& T, FSmem& S,
                                int q, int* s_flag) {
   constexpr int BSQ = NTQ * 8;
   const int rows = sl.rows, cols = A.cols, ldy = T.ldy;
@@ -816,6 +972,20 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
   const double* gb = A.G.buf + (long long)s * A.G.cap;
   const int kA = sl.kA, K = A.K, KW = kA + K;
   const int ldw = (KW + 1) & ~1;
+  // TMA staging for the sampling products: after the bs-column Y panel, inside
+  // the (FUSED_QMAX-column) panel region that recompression uses later
+  __shared__ __align__(8) uint64_t s_sbar[2];
+  Stager stg{nullptr, s_sbar};
+  unsigned sph = 0;
+  const bool use_tma = A.stage && NT <= 2 && cols <= MAXROWS && rows <= MAXROWS;
+  if (use_tma) {
+    stg.buf = S.Y + (((long long)ldy * bs + 15) & ~15LL);
+    if (threadIdx.x == 0) {
+      mbar_init(&s_sbar[0], 1);
+      mbar_init(&s_sbar[1], 1);
+    }
+    cbar();
+  }
 
   long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = clock64(), t_begin = t_prev;
@@ -865,18 +1035,25 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
           rows, cols, [&](int k) { return sl.Ad + (long long)k * sl.ldad; }, Om, cols,
           [&](int m, int n, double v) { S.Y[m + n * ldy] = v; });
     } else {
-      // W = [V^A | -U_k,:]^T Omega   (KW x bs, ld ldw)
-      tn16<NT>(
-          KW, cols,
-          [&](int m) { return m < kA ? sl.VA + (long long)m * cols : A.Ucat + (long long)(m - kA) * cols; },
-          [&](int n) { return Om + (long long)n * cols; },
-          [&](int m) { return m < kA ? 1.0 : -1.0; },
-          [&](int m, int n, double v) { sl.W[m + (long long)n * ldw] = v; }, S.part);
-      // Y = [U^A | H] W
-      nn16<NT>(
-          rows, KW,
-          [&](int k) { return k < kA ? sl.UA + (long long)k * rows : sl.H + (long long)(k - kA) * rows; },
-          sl.W, ldw, [&](int m, int n, double v) { S.Y[m + n * ldy] = v; });
+      auto acolW = [&](int m) {
+        return m < kA ? sl.VA + (long long)m * cols : A.Ucat + (long long)(m - kA) * cols;
+      };
+      auto acolY = [&](int k) {
+        return k < kA ? sl.UA + (long long)k * rows : sl.H + (long long)(k - kA) * rows;
+      };
+      auto sgnW = [&](int m) { return m < kA ? 1.0 : -1.0; };
+      auto outW = [&](int m, int n, double v) { sl.W[m + (long long)n * ldw] = v; };
+      auto epiY = [&](int m, int n, double v) { S.Y[m + n * ldy] = v; };
+      if (use_tma) {
+        // W = [V^A | -U_k,:]^T Omega   (KW x bs, ld ldw), then Y = [U^A | H] W
+        tn16_tma<NT>(KW, cols, acolW, [&](int n) { return Om + (long long)n * cols; }, sgnW, outW,
+                     S.part, stg, sph);
+        nn16_tma<NT>(rows, KW, acolY, sl.W, ldw, epiY, stg, sph);
+      } else {
+        tn16<NT>(KW, cols, acolW, [&](int n) { return Om + (long long)n * cols; }, sgnW, outW,
+                 S.part);
+        nn16<NT>(rows, KW, acolY, sl.W, ldw, epiY);
+      }
     }
     tick(1);
     // ---- orthog (dense_kernels.cpp:379-420) ------------------------------------
@@ -994,6 +1171,7 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
 size_t fused_smem_bytes(int maxrows, int bs, int window, int* ldy, long long* ysz) {
   int l = ((maxrows + 15) / 16) * 16 + 4;
   long long y = (long long)l * std::max(bs, FUSED_QMAX);
+  if (bs <= 16) y = std::max(y, (((long long)l * bs + 15) & ~15LL) + 2LL * SCOL * SPAD);
   y = (y + 1) & ~1LL;
   *ldy = l;
   *ysz = y;
@@ -1029,6 +1207,12 @@ void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st) {
   size_t bytes = fused_smem_bytes(maxrows, bs, args.window, &args.ldy, &ysz);
   args.ysz = ysz;
   args.stg_half = 0;
+  {
+    // TMA-staged sampling operands: correct, but measured slower than the direct
+    // 128-bit fragment loads at cfg2 (per-chunk barriers dominate) -> opt-in
+    const char* e = std::getenv("TLRG_FUSED_TMA");
+    args.stage = (bs <= 16 && e && e[0] == '1') ? 1 : 0;
+  }
   switch (bs) {
 #define TLRG_FUSED_CASE(NT)                                                                 \
   case NT * 8: {                                                                            \

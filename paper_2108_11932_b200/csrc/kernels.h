@@ -199,6 +199,7 @@ struct FusedArgs {
   int* rank_out;       // final rank, or -1 when the tile needs the batched fallback
   double* flops_out;   // per slot: algorithmic FP64 flops executed by the CTA
   int mgs_passes;      // column passes per sweep in the panel MGS (reference: 2)
+  int stage;           // TMA-stage the sampling operands (set by the launcher)
 };
 constexpr int FUSED_QMAX = 32;  // widest basis recompressed in-kernel
 bool ara_fused_supported(int maxrows, int bs, int window);
