@@ -472,18 +472,11 @@ __global__ void __launch_bounds__(BK_T) sytrf_bk_kernel(double* A, int n, double
       double akk = a(k, k);
       if (akk != 0.0) {
         double r1 = 1.0 / akk;
-        // trailing rank-1 update (dsyr, lower) then scale the column
-        int m = n - k - 1;
-        long long tot = (long long)m * (m + 1) / 2;
-        for (long long t = tid; t < tot; t += BK_T) {
-          // map t -> (i, j) with j <= i in the trailing (m x m) lower triangle
-          int jj = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) / 2.0);
-          while ((long long)jj * (jj + 1) / 2 > t) --jj;
-          while ((long long)(jj + 1) * (jj + 2) / 2 <= t) ++jj;
-          int ii = (int)(t - (long long)jj * (jj + 1) / 2);
-          // (row = jj, col = ii) in lower triangle: i = k+1+jj, j = k+1+ii
-          int i = k + 1 + jj, j = k + 1 + ii;
-          a(i, j) -= r1 * a(i, k) * a(j, k);
+        // trailing rank-1 update (dsyr, lower) then scale the column: one warp
+        // per column j, lanes over rows i >= j (coalesced, no index arithmetic)
+        for (int j = k + 1 + warp; j < n; j += nw) {
+          const double ajk = r1 * a(j, k);
+          for (int i = j + lane; i < n; i += 32) a(i, j) -= a(i, k) * ajk;
         }
         __syncthreads();
         for (int i = k + 1 + tid; i < n; i += BK_T) a(i, k) *= r1;
@@ -496,17 +489,10 @@ __global__ void __launch_bounds__(BK_T) sytrf_bk_kernel(double* A, int n, double
         double d22 = a(k, k) / d21;
         double t = 1.0 / (d11 * d22 - 1.0);
         d21 = t / d21;
-        int m = n - k - 2;
-        long long tot = (long long)m * (m + 1) / 2;
-        for (long long q = tid; q < tot; q += BK_T) {
-          int jj = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) / 2.0);
-          while ((long long)jj * (jj + 1) / 2 > q) --jj;
-          while ((long long)(jj + 1) * (jj + 2) / 2 <= q) ++jj;
-          int ii = (int)(q - (long long)jj * (jj + 1) / 2);
-          int i = k + 2 + jj, j = k + 2 + ii;
-          double wkj = d21 * (d11 * a(j, k) - a(j, k + 1));
-          double wkp1j = d21 * (d22 * a(j, k + 1) - a(j, k));
-          a(i, j) -= a(i, k) * wkj + a(i, k + 1) * wkp1j;
+        for (int j = k + 2 + warp; j < n; j += nw) {
+          const double wkj = d21 * (d11 * a(j, k) - a(j, k + 1));
+          const double wkp1j = d21 * (d22 * a(j, k + 1) - a(j, k));
+          for (int i = j + lane; i < n; i += 32) a(i, j) -= a(i, k) * wkj + a(i, k + 1) * wkp1j;
         }
         __syncthreads();
         for (int j = k + 2 + tid; j < n; j += BK_T) {
