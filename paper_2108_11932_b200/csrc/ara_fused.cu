@@ -279,10 +279,12 @@ struct TileCtx {
 
 // Reduce-scatter of N (16 or 32) values over a warp: afterwards every lane
 // holds the full warp sum of index (lane >> 1) (N = 16) or lane (N = 32).
+// Reduce-scatter of N (a power of two <= 32) values over a warp: afterwards
+// every lane holds the full warp sum of index lane >> (5 - log2 N).  N halving
+// levels (N-1 shuffles) plus one full xor level per remaining lane bit.
 template <int N>
 __device__ __forceinline__ double warp_reduce_scatter(double (&v)[N]) {
   const int lane = threadIdx.x & 31;
-  int base = 0;
   double w[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) w[i] = v[i];
@@ -295,10 +297,10 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[N]) {
       const double keep = hi ? w[i + half] : w[i];
       w[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
     }
-    base += hi ? half : 0;
   }
   double r = w[0];
-  if (N == 16) r += __shfl_xor_sync(0xffffffffu, r, 1);
+#pragma unroll
+  for (int bit = 16 / N; bit >= 1; bit >>= 1) r += __shfl_xor_sync(0xffffffffu, r, bit);
   return r;
 }
 
@@ -467,7 +469,8 @@ template <int BS, int J>
 __device__ __forceinline__ void cgs_pass_reg(double (&y)[RPT][BS], FSmem& S, double* rpj,
                                              int& par) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int N = J <= 16 ? 16 : 32;
+  constexpr int N = J <= 2 ? 2 : J <= 4 ? 4 : J <= 8 ? 8 : J <= 16 ? 16 : 32;
+  constexpr int SH = (N == 2 ? 4 : N == 4 ? 3 : N == 8 ? 2 : N == 16 ? 1 : 0);  // 5 - log2 N
   double part[N];
 #pragma unroll
   for (int p = 0; p < N; ++p) {
@@ -481,11 +484,7 @@ __device__ __forceinline__ void cgs_pass_reg(double (&y)[RPT][BS], FSmem& S, dou
   const double red = warp_reduce_scatter<N>(part);
   double* wp = S.wpart + par * (FW * 32);
   par ^= 1;
-  if (N == 32) {
-    wp[warp * 32 + lane] = red;
-  } else if ((lane & 1) == 0) {
-    wp[warp * 32 + (lane >> 1)] = red;
-  }
+  if ((lane & ((1 << SH) - 1)) == 0) wp[warp * 32 + (lane >> SH)] = red;
   cbar();
   double c = 0.0;
   if (lane < J) {
