@@ -104,7 +104,7 @@ __device__ void tn16(int M, int Kd, ACol acol, BCol bcol, Sgn sgn, Out out, doub
       for (int i = 0; i < MTW; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll 2
+#pragma unroll 4
       for (int kb = 0; kb < k8; ++kb) {
         const int kk = kb * 8 + 2 * t;
         const bool kv = kk < Kd;
@@ -216,7 +216,7 @@ __device__ void nn16(int rows, int Kd, ACol acol, const double* B, int ldb, Epi 
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
   const int k8 = (Kd + 7) / 8;
-#pragma unroll 2
+#pragma unroll 4
   for (int kb = 0; kb < k8; ++kb) {
     const int kk = kb * 8 + 2 * t;
     double2 aw[NT];

@@ -61,7 +61,7 @@ std::unique_ptr<Matrix> build_tlr_device(Ctx& C, int dim, int64_t n, const doubl
   M->rank.assign(nt, 0);
   M->U.assign(nt, nullptr);
   M->V.assign(nt, nullptr);
-  TLRG_CUDA(cudaMalloc(&M->diag, sizeof(double) * (size_t)nb * b * b));
+  TLRG_CUDA(cudaMallocAsync(&M->diag, sizeof(double) * (size_t)nb * b * b, C.st_main));
   double* X = C.buf<double>("bt_X", (size_t)n * dim);
   TLRG_CUDA(cudaMemcpyAsync(X, coords_host, 8 * (size_t)n * dim, cudaMemcpyHostToDevice, C.st));
   int* bad = C.buf<int>("bt_bad", 1);
@@ -83,6 +83,8 @@ std::unique_ptr<Matrix> build_tlr_device(Ctx& C, int dim, int64_t n, const doubl
     eval(d);
   }
   auto S = std::make_shared<Store>();
+  S->st = C.st_main;
+  S->owner = &C;
   M->stores.push_back(S);
   AraCfg cfg = cfg_in;
   cfg.eps = eps;

@@ -79,7 +79,7 @@ std::unique_ptr<Matrix> upload(Ctx& C, int64_t n, int b, double eps, const doubl
   M->rank.assign(nt, 0);
   M->U.assign(nt, nullptr);
   M->V.assign(nt, nullptr);
-  TLRG_CUDA(cudaMalloc(&M->diag, sizeof(double) * (size_t)nb * b * b));
+  TLRG_CUDA(cudaMallocAsync(&M->diag, sizeof(double) * (size_t)nb * b * b, C.st_main));
   if (diag && n % b == 0) {
     TLRG_CUDA(cudaMemcpyAsync(M->diag, diag, sizeof(double) * (size_t)nb * b * b,
                               cudaMemcpyHostToDevice, C.st));
@@ -104,6 +104,8 @@ std::unique_ptr<Matrix> upload(Ctx& C, int64_t n, int b, double eps, const doubl
       totV += (size_t)M->rows(j) * r;
     }
   auto S = std::make_shared<Store>();
+  S->st = C.st_main;
+  S->owner = &C;
   M->stores.push_back(S);
   double* dU = totU ? S->alloc(totU) : nullptr;
   double* dV = totV ? S->alloc(totV) : nullptr;
@@ -186,7 +188,7 @@ std::unique_ptr<Matrix> clone(Ctx& C, const Matrix& M) {
   R->U.assign(M.U.size(), nullptr);
   R->V.assign(M.V.size(), nullptr);
   size_t dbytes = sizeof(double) * (size_t)M.nb * M.b * M.b;
-  TLRG_CUDA(cudaMalloc(&R->diag, dbytes));
+  TLRG_CUDA(cudaMallocAsync(&R->diag, dbytes, C.st_main));
   TLRG_CUDA(cudaMemcpyAsync(R->diag, M.diag, dbytes, cudaMemcpyDeviceToDevice, C.st));
   size_t tot = 0;
   for (int i = 1; i < M.nb; ++i)
@@ -195,6 +197,8 @@ std::unique_ptr<Matrix> clone(Ctx& C, const Matrix& M) {
       tot += (size_t)(M.rows(i) + M.rows(j)) * r;
     }
   auto S = std::make_shared<Store>();
+  S->st = C.st_main;
+  S->owner = &C;
   R->stores.push_back(S);
   double* base = tot ? S->alloc(tot) : nullptr;
   size_t o = 0;
@@ -284,6 +288,15 @@ int tlrg_create(int device, tlrg_ctx* out, tlrg_status* st) {
     TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.st2, cudaStreamNonBlocking));
     TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.sd, cudaStreamNonBlocking));
     c->c.st_main = c->c.st;
+    ctx_register(&c->c, true);
+    {
+      // stream-ordered allocations for matrices / panels: keep freed blocks in
+      // the pool (no synchronous cudaFree in the factorization loop)
+      cudaMemPool_t pool;
+      TLRG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t thr = ~0ULL;
+      TLRG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     c->c.desc.reserve(16 << 20);
     // one-time kernel attribute setup (never inside a graph capture)
     panel_mgs(nullptr, 0, 0, 0, 1, 1, c->c.st);

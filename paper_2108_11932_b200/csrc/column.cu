@@ -10,7 +10,9 @@
 //                  recompression.
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <numeric>
+#include <set>
 
 #include "core.h"
 
@@ -373,12 +375,36 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
 }
 
 // ----------------------------------------------------------------- Store ---
+namespace {
+std::mutex& ctx_mu() {
+  static std::mutex m;
+  return m;
+}
+std::set<const void*>& ctx_set() {
+  static std::set<const void*> s;
+  return s;
+}
+}  // namespace
+bool ctx_alive(const void* ctx) {
+  std::lock_guard<std::mutex> lk(ctx_mu());
+  return ctx && ctx_set().count(ctx);
+}
+void ctx_register(const void* ctx, bool alive) {
+  std::lock_guard<std::mutex> lk(ctx_mu());
+  if (alive) ctx_set().insert(ctx);
+  else ctx_set().erase(ctx);
+}
+void stream_free(const void* ctx, cudaStream_t st, void* p) {
+  if (!p) return;
+  if (st && ctx_alive(ctx)) cudaFreeAsync(p, st);
+  else cudaFree(p);
+}
 double* Store::alloc(size_t n) {
   n = (n + 31) & ~(size_t)31;  // 256-byte granules
   if (!cur || used + n > cap) {
     size_t c = std::max(n, (size_t)1 << 23);  // >= 64 MiB chunks
     void* p = nullptr;
-    TLRG_CUDA(cudaMalloc(&p, c * sizeof(double)));
+    TLRG_CUDA(cudaMallocAsync(&p, c * sizeof(double), st));
     chunks.push_back(p);
     cur = static_cast<double*>(p);
     cap = c;
@@ -390,7 +416,7 @@ double* Store::alloc(size_t n) {
   return r;
 }
 Store::~Store() {
-  for (void* p : chunks) cudaFree(p);
+  for (void* p : chunks) stream_free(owner, st, p);
 }
 
 }  // namespace tlrg

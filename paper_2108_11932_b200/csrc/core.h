@@ -46,7 +46,15 @@ struct DevBuf {
 };
 
 // Device memory for low-rank payloads (append-only chunks, never moved).
+// Live contexts: stream-ordered frees go to the owner's stream only while it
+// exists (Python may collect a matrix after its context); otherwise cudaFree.
+bool ctx_alive(const void* ctx);
+void ctx_register(const void* ctx, bool alive);
+void stream_free(const void* ctx, cudaStream_t st, void* p);
+
 struct Store {
+  cudaStream_t st = nullptr;  // stream-ordered pool allocations (set by the owner)
+  const void* owner = nullptr;
   std::vector<void*> chunks;
   double* cur = nullptr;
   size_t cap = 0, used = 0;

@@ -376,6 +376,8 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     TLRG_CUDA(cudaMemsetAsync(F->D.s2, 0, nb * b, C.st));
   }
   auto store = std::make_shared<Store>();
+  store->st = C.st_main;
+  store->owner = &C;
   M.stores.push_back(store);
   double* Dk = C.buf<double>("Dk", (size_t)b * b);
   double* a0 = C.buf<double>("akk0", (size_t)b * b);

@@ -464,6 +464,8 @@ double* Ctx::pinned_dbl(size_t n) {
   return h_dbl;
 }
 Ctx::~Ctx() {
+  ctx_register(this, false);
+  if (st_main) cudaStreamSynchronize(st_main);
   if (h_ints) cudaFreeHost(h_ints);
   if (h_dbl) cudaFreeHost(h_dbl);
   bufs.clear();
@@ -473,7 +475,7 @@ Ctx::~Ctx() {
   for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
 }
 void Matrix::free_all() {
-  if (diag) cudaFree(diag);
+  if (diag) stream_free(ctx, ctx_alive(ctx) ? ctx->st_main : nullptr, diag);
   diag = nullptr;
   stores.clear();
 }
