@@ -290,8 +290,10 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
   sv[0] = SvdTask{};
   sv[0].A = Bm; sv[0].V = Vm; sv[0].sig = sig; sv[0].work = work; sv[0].rank_out = rank_out;
   sv[0].n = p; sv[0].cut = eps;
-  sv[0].tol = 1e-11;  // eigenvectors to 1e-11: ample for the eps-level split, 2 fewer sweeps
-  jacobi_svd(C.push(sv), 1, p, C.st);
+  sv[0].tol = 1e-14;  // off-diagonals below 1e-14 ||B||_F: ample for the eps-level split
+  // symmetric PSD core: two-sided Jacobi (no dot products; 3 barriers a step)
+  if (p <= 64) sym_jacobi(C.push(sv), 1, p, C.st);
+  else jacobi_svd(C.push(sv), 1, p, C.st);
   ++C.launches;
   // R = D - (Q A_B)(Q V_B)^T restricted to the r = *rank_out retained directions
   double* Xl = C.buf<double>("sc_Xl", (size_t)n * p);

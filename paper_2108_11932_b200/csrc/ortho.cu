@@ -341,16 +341,23 @@ __global__ void __launch_bounds__(SJ_T) sym_jacobi_kernel(SvdTask* tasks) {
     s_fro = sqrt(f);
   }
   __syncthreads();
-  const double tol_abs = 2.220446049250313e-16 * s_fro;
+  const double tol_abs = (T.tol > 0.0 ? T.tol : 2.220446049250313e-16) * s_fro;
   const int nn = n + (n & 1), np = nn / 2;
+  const int lane = tid & 31, warp = tid >> 5;
   for (int sweep = 0; sweep < 30; ++sweep) {
     if (tid == 0) s_rot = 0;
     for (int step = 0; step < nn - 1; ++step) {
-      // rotation parameters, one thread per pair
-      for (int pi = tid; pi < np; pi += SJ_T) {
-        int p = (step + pi) % (nn - 1);
-        int q = pi == 0 ? nn - 1 : (step - pi + nn - 1) % (nn - 1);
-        if (p > q) { const int t = p; p = q; q = t; }
+      // rotation parameters, one thread per pair (round-robin ordering)
+      if (tid < np) {
+        const int pi = tid;
+        int p = step + pi;
+        if (p >= nn - 1) p -= nn - 1;
+        int q = nn - 1;
+        if (pi != 0) {
+          q = step - pi;
+          if (q < 0) q += nn - 1;
+        }
+        if (p > q) { const int t2 = p; p = q; q = t2; }
         double c = 1.0, sn = 0.0;
         if (q < n) {
           const double bpq = B[p * ld + q];
@@ -365,32 +372,36 @@ __global__ void __launch_bounds__(SJ_T) sym_jacobi_kernel(SvdTask* tasks) {
         rc[pi] = c;
         rs[pi] = sn;
         rp[pi] = p;
-        rq[pi] = q < n ? q : -1;
+        rq[pi] = (q < n && sn != 0.0) ? q : -1;
       }
       __syncthreads();
-      // rows p, q of B
-      for (int e = tid; e < np * n; e += SJ_T) {
-        const int pi = e / n, k = e % n, q = rq[pi];
-        if (q < 0 || rs[pi] == 0.0) continue;
+      // rows p, q of B: warp per pair, lanes over columns (no index division)
+      for (int pi = warp; pi < np; pi += SJ_T / 32) {
+        const int q = rq[pi];
+        if (q < 0) continue;
         const int p = rp[pi];
         const double c = rc[pi], sn = rs[pi];
-        const double x = B[p * ld + k], y = B[q * ld + k];
-        B[p * ld + k] = c * x - sn * y;
-        B[q * ld + k] = sn * x + c * y;
+        for (int k = lane; k < n; k += 32) {
+          const double x = B[p * ld + k], y = B[q * ld + k];
+          B[p * ld + k] = c * x - sn * y;
+          B[q * ld + k] = sn * x + c * y;
+        }
       }
       __syncthreads();
       // columns p, q of B and of V
-      for (int e = tid; e < np * n; e += SJ_T) {
-        const int pi = e / n, k = e % n, q = rq[pi];
-        if (q < 0 || rs[pi] == 0.0) continue;
+      for (int pi = warp; pi < np; pi += SJ_T / 32) {
+        const int q = rq[pi];
+        if (q < 0) continue;
         const int p = rp[pi];
         const double c = rc[pi], sn = rs[pi];
-        const double x = B[k * ld + p], y = B[k * ld + q];
-        B[k * ld + p] = c * x - sn * y;
-        B[k * ld + q] = sn * x + c * y;
-        const double vx = V[k * ld + p], vy = V[k * ld + q];
-        V[k * ld + p] = c * vx - sn * vy;
-        V[k * ld + q] = sn * vx + c * vy;
+        for (int k = lane; k < n; k += 32) {
+          const double x = B[k * ld + p], y = B[k * ld + q];
+          B[k * ld + p] = c * x - sn * y;
+          B[k * ld + q] = sn * x + c * y;
+          const double vx = V[k * ld + p], vy = V[k * ld + q];
+          V[k * ld + p] = c * vx - sn * vy;
+          V[k * ld + q] = sn * vx + c * vy;
+        }
       }
       __syncthreads();
     }

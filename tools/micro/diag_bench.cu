@@ -69,14 +69,14 @@ int main() {
     cudaMalloc(&dS, 8 * p);
     cudaMalloc(&dWk, 16 * p * p);
     cudaMalloc(&rk, 4);
-    t.A = dG; t.V = dV; t.sig = dS; t.work = dWk; t.rank_out = rk; t.n = p; t.cut = 1e-2;
+    t.A = dG; t.V = dV; t.sig = dS; t.work = dWk; t.rank_out = rk; t.n = p; t.cut = 1e-2; t.tol = 1e-14;
     SvdTask* dt;
     cudaMalloc(&dt, sizeof(SvdTask));
     cudaMemcpy(dt, &t, sizeof t, cudaMemcpyHostToDevice);
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemcpy(dG, G.data(), 8 * p * p, cudaMemcpyHostToDevice);
       cudaEventRecord(a, st);
-      jacobi_svd(dt, 1, p, st);
+      if (p <= 64) sym_jacobi(dt, 1, p, st); else jacobi_svd(dt, 1, p, st);
       cudaEventRecord(b, st);
       cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms, a, b);
