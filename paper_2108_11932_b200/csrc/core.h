@@ -23,7 +23,6 @@ struct Error : std::runtime_error {
 [[noreturn]] inline void data_error(const std::string& m) { throw Error(3, m); }
 [[noreturn]] inline void numeric_error(const std::string& m, int idx) { throw Error(4, m, idx); }
 
-void release_retired_arenas();
 
 // Grow-only device scratch buffer.  Only resized at synchronisation points.
 struct DevBuf {
@@ -133,7 +132,7 @@ struct Ctx {
     if (sd) TLRG_CUDA(cudaStreamSynchronize(sd));
     if (st_main && st_main != st) TLRG_CUDA(cudaStreamSynchronize(st_main));
     desc.reset();
-    release_retired_arenas();
+    desc.release_retired();
     if (!ev_pending.empty()) drain_events();
   }
   // wait for the current stream only (no arena recycling): other streams keep

@@ -662,9 +662,9 @@ static double* trsm_scratch(size_t n) {
 
 void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
                 const double* d, const double* e, const uint8_t* s2, int* info,
-                cudaStream_t st) {
+                cudaStream_t st, double* work) {
   if (nrhs <= 0 || n <= 0) return;
-  double* W = perm ? trsm_scratch((size_t)n * nrhs) : nullptr;
+  double* W = perm ? (work ? work : trsm_scratch((size_t)n * nrhs)) : nullptr;
   const int nt = (n + 31) / 32;
   const long long ncc = (nrhs + 31) / 32;
   long long want = std::max<long long>(ncc, (long long)(nt - 1) * ncc);

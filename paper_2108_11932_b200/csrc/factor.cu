@@ -440,7 +440,8 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       } else {
         size_t o = (size_t)k * b;
         trsm_panel(diagk, rk, Xinv, rk, F->D.perm + o, F->D.d + o, F->D.e + o, F->D.s2 + o,
-                   info + 3, C.st);
+                   info + 3, C.st,
+                   C.buf<double>("trsm_W", (size_t)rk * rk));
         min_block_pivot(F->D.d + o, F->D.e + o, F->D.s2 + o, rk, piv + k, C.st);
       }
       C.launches += 3;

@@ -7,20 +7,10 @@
 
 namespace tlrg {
 
-namespace {
-struct Retired {
-  char* h;
-  char* d;
-};
-std::vector<Retired>& retired() {
-  static std::vector<Retired> r;
-  return r;
-}
-}  // namespace
 
 void DescArena::reserve(size_t bytes) {
   if (bytes <= cap) return;
-  if (h) retired().push_back({h, d});  // freed at the next reset-safe point
+  if (h) retired.push_back({h, d});  // freed at the owner's next reset-safe point
   size_t c = std::max(bytes, (size_t)1 << 20);
   TLRG_CUDA(cudaMallocHost(&h, c));
   TLRG_CUDA(cudaMalloc(&d, c));
@@ -33,7 +23,7 @@ void* DescArena::push(const void* src, size_t bytes, cudaStream_t st) {
   if (off + bytes > cap) {
     // Old block may still be read by in-flight kernels: retire it, never free
     // it before the owner synchronises.
-    if (h) retired().push_back({h, d});
+    if (h) retired.push_back({h, d});
     size_t c = std::max(2 * cap, bytes + 256);
     c = std::max(c, (size_t)1 << 20);
     TLRG_CUDA(cudaMallocHost(&h, c));
@@ -48,16 +38,17 @@ void* DescArena::push(const void* src, size_t bytes, cudaStream_t st) {
 }
 
 DescArena::~DescArena() {
+  release_retired();
   if (h) cudaFreeHost(h);
   if (d) cudaFree(d);
 }
 
-void release_retired_arenas() {
-  for (auto& r : retired()) {
+void DescArena::release_retired() {
+  for (auto& r : retired) {
     cudaFreeHost(r.h);
     cudaFree(r.d);
   }
-  retired().clear();
+  retired.clear();
 }
 
 template <int BM, int BN>

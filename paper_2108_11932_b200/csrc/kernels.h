@@ -28,12 +28,18 @@ void gemm_launch(const GemmPlan& p, cudaStream_t st);
 // Device scratch for kernel argument tables: pinned host staging + device
 // mirror, bump-allocated and reset by the owner after a stream sync.
 struct DescArena {
+  struct Retired {
+    char* h;
+    char* d;
+  };
   char* h = nullptr;
   char* d = nullptr;
   size_t cap = 0, used = 0;
+  std::vector<Retired> retired;  // outgrown blocks, freed at the owner's next full sync
   void reserve(size_t bytes);
   void* push(const void* src, size_t bytes, cudaStream_t st);  // returns device ptr
   void reset() { used = 0; }
+  void release_retired();
   ~DescArena();
 };
 
@@ -215,7 +221,7 @@ void sytrf_bk(double* A, int n, double* d, double* e, uint8_t* s2, int* perm, in
 // X <- L^{-1} B (Chol) or X <- D^{-1} Lunit^{-1} P B (LDL), B rows x nrhs (ld rows).
 void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* perm,
                 const double* d, const double* e, const uint8_t* s2, int* info,
-                cudaStream_t st);
+                cudaStream_t st, double* work = nullptr /* n x nrhs, LDL mode */);
 // (shifted) Cholesky-QR step: R^T R = G (+ shift), Rinv = R^{-1}, p <= 160
 void cholqr_factor(const double* G, int p, int n, int shift, double* Rinv, cudaStream_t st);
 // Y (n x p, ld n) <- Y R^{-1} row by row (R upper p x p from cholqr_factor's

@@ -58,3 +58,24 @@ def test_split_column_factor_is_bitwise_identical(tg, ref, world, eps, bs):
             assert np.array_equal(a, b_)
         for a, b_ in zip(V, V1):
             assert np.array_equal(a, b_)
+
+
+def test_split_column_ldlt_is_bitwise_identical(tg, ref):
+    """LDL^T: D blocks and the intra-tile permutations are computed redundantly
+    on every rank, the panels exchanged; factors equal bitwise to 1 rank."""
+    from paper_2108_11932_b200 import geometry as G
+    pts = points(G.GRID2D, 1024, 128)
+    A_ref = ref.build(pts, 1, 0.2, 1e-4, 128, 1e-5, 0, 16, 3)
+    parts = A_ref.to_parts()
+    cfg = tg.AraConfig(block_samples=16, eps=1e-5, seed=3)
+    F1 = tg.tlr_ldlt(tg.TlrMatrix.from_parts(1024, 128, 1e-5, *parts), cfg)
+    d1, r1, U1, V1 = F1.L.to_parts()
+    for F in _factor_ranks(tg, parts, 1024, 128, 1e-5, cfg, 2, mode=1):
+        d, r, U, V = F.L.to_parts()
+        assert (np.asarray(r) == np.asarray(r1)).all()
+        assert all(np.array_equal(a, b_) for a, b_ in zip(d, d1))
+        assert all(np.array_equal(a, b_) for a, b_ in zip(V, V1))
+        for k in range(F.L.nb):
+            (Da, pa), (Db, pb) = F.dblock(k), F1.dblock(k)
+            assert np.array_equal(pa, pb)
+            assert np.array_equal(Da.d, Db.d) and np.array_equal(Da.e, Db.e)
