@@ -62,8 +62,7 @@ bool ara_fused_eligible(int cols, const std::vector<int>& rows, int bs, int wind
   if (nf && nf[0] == '1') return false;
   // bs = 32 (configs 3-5): the per-tile products are heavy enough that the
   // batched multi-CTA GEMMs of the graph path win (measured at config 3)
-  const char* ff = std::getenv("TLRG_FORCE_FUSED");
-  if (bs > 16 && !(ff && ff[0] == '1')) return false;
+  if (bs > 16) return false;
   if (cols % 2) return false;
   int maxrows = 0;
   for (int r : rows) {

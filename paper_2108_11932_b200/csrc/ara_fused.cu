@@ -1186,7 +1186,9 @@ size_t fused_smem_bytes(int maxrows, int bs, int window, int* ldy, long long* ys
 
 bool ara_fused_supported(int maxrows, int bs, int window) {
   if (maxrows > MAXROWS) return false;  // callers also need even rows / cols
-  if (bs != 8 && bs != 16 && bs != 24 && bs != 32) return false;
+  // bs = 24 / 32 take the graph path (measured faster there; see ara.cu), so
+  // only the 8- and 16-column instances are compiled
+  if (bs != 8 && bs != 16) return false;
   int ldy;
   long long ysz;
   size_t bytes = fused_smem_bytes(maxrows, bs, window, &ldy, &ysz);
@@ -1222,8 +1224,6 @@ void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st) {
   }
     TLRG_FUSED_CASE(1)
     TLRG_FUSED_CASE(2)
-    TLRG_FUSED_CASE(3)
-    TLRG_FUSED_CASE(4)
 #undef TLRG_FUSED_CASE
     default:
       throw CudaError("ara_fused: unsupported block size");
