@@ -32,12 +32,17 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if not force and os.path.exists(so) and \
             os.path.getmtime(so) >= max(os.path.getmtime(p) for p in deps):
         return so
+    hdr_t = max(os.path.getmtime(p) for p in deps if not p.endswith(".cu"))
     objs = []
     jobs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         for s in srcs:
             o = os.path.join(OUT, os.path.basename(s)[:-3] + ".o")
             objs.append(o)
+            # per-object rebuild: a source edit recompiles only its own object
+            if not force and os.path.exists(o) and \
+                    os.path.getmtime(o) >= max(os.path.getmtime(s), hdr_t):
+                continue
             cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
             jobs.append(ex.submit(_run, cmd))
         for j in jobs:

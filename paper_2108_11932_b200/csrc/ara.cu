@@ -14,6 +14,7 @@
 // + one-sided Jacobi SVD of R, cut at (1 - 1/eta) eps) in batches, and the
 // final factors are written into a contiguous panel.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
@@ -473,6 +474,13 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
 
   // ---- recompression (ara.cpp:201-211) --------------------------------------
   tr.start(C.st);
+  const char* rpe = std::getenv("TLRG_RECPROF");
+  const bool recprof = rpe && rpe[0] == '1';
+  auto hnow = [] { return std::chrono::steady_clock::now(); };
+  auto hms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  auto h0 = hnow(), h1 = h0, h2 = h0, h3 = h0, h4 = h0;
   std::vector<int> fr(T, 0);
   const double cut = (1.0 - 1.0 / cfg.safety) * cfg.eps;
   const bool recomp = cfg.recompress && cut > 0.0;
@@ -512,6 +520,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
         }
       ensure(need_s, need);
     }
+    h1 = hnow();
     for (int s = 0; s < T; ++s) {
       if (q[s] == 0) continue;
       PanelTask P{};
@@ -549,9 +558,11 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     panel_mgs(d_tasks, (int)tasks.size(), 1, 1, qmax, cols, C.st);
     jacobi_svd(C.push(svd), (int)svd.size(), qmax, C.st);
     C.launches += 4;
+    h2 = hnow();
     std::vector<int> hr(T);
     TLRG_CUDA(cudaMemcpyAsync(hr.data(), rko, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
     C.wait();
+    h3 = hnow();
     for (int s : sl) fr[s] = hr[s];
   } else {
     for (int s = 0; s < T; ++s) fr[s] = q[s];
@@ -568,6 +579,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   // [U panel | V panel] in one allocation (one contiguous multi-GPU send buffer)
   double* Up = (utot + vtot) ? store.alloc((size_t)(utot + vtot)) : nullptr;
   double* Vp = vtot ? Up + utot : nullptr;
+  h4 = hnow();
   std::vector<GemmProblem> pu;
   std::vector<CopyItem> cpy;
   long long uo = 0, vo = 0;
@@ -610,6 +622,15 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   }
   tr.stop(C.st);
   C.wait();
+  if (recprof && qmax > 0) {
+    int nf = 0;
+    for (int s = 0; s < T; ++s) nf += q[s] > 0;
+    std::fprintf(stderr,
+                 "recomp fallback tiles %d qmax %d | host: setup+ensure %.3f launch %.3f wait %.3f "
+                 "alloc %.3f rest %.3f | dev %.3f ms\n",
+                 nf, qmax, hms(h0, h1), hms(h1, h2), hms(h2, h3), hms(h3, h4), hms(h4, hnow()),
+                 tr.sec() * 1e3);
+  }
   cst.t_projection += tp.sec();
   cst.t_recompress += tr.sec();
 }

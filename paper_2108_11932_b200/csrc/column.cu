@@ -14,6 +14,8 @@
 #include <numeric>
 #include <set>
 
+#include <unordered_map>
+
 #include "core.h"
 
 namespace tlrg {
@@ -399,13 +401,58 @@ void stream_free(const void* ctx, cudaStream_t st, void* p) {
   if (st && ctx_alive(ctx)) cudaFreeAsync(p, st);
   else cudaFree(p);
 }
+namespace {
+constexpr size_t kChunk = (size_t)1 << 23;  // 64 MiB of doubles
+std::mutex& chunk_mu() {
+  static std::mutex m;
+  return m;
+}
+std::unordered_map<const void*, std::vector<void*>>& chunk_cache() {
+  static std::unordered_map<const void*, std::vector<void*>> c;
+  return c;
+}
+}  // namespace
+void chunk_cache_release(const void* ctx) {
+  std::vector<void*> v;
+  {
+    std::lock_guard<std::mutex> lk(chunk_mu());
+    auto it = chunk_cache().find(ctx);
+    if (it == chunk_cache().end()) return;
+    v.swap(it->second);
+    chunk_cache().erase(it);
+  }
+  for (void* p : v) cudaFree(p);
+}
+void chunk_cache_reserve(const void* ctx, size_t doubles, cudaStream_t st) {
+  const size_t need = (doubles + kChunk - 1) / kChunk;
+  size_t have;
+  {
+    std::lock_guard<std::mutex> lk(chunk_mu());
+    have = chunk_cache()[ctx].size();
+  }
+  for (; have < need; ++have) {
+    void* p = nullptr;
+    TLRG_CUDA(cudaMallocAsync(&p, kChunk * sizeof(double), st));
+    std::lock_guard<std::mutex> lk(chunk_mu());
+    chunk_cache()[ctx].push_back(p);
+  }
+}
 double* Store::alloc(size_t n) {
   n = (n + 31) & ~(size_t)31;  // 256-byte granules
   if (!cur || used + n > cap) {
-    size_t c = std::max(n, (size_t)1 << 23);  // >= 64 MiB chunks
+    const size_t c = std::max(n, kChunk);  // >= 64 MiB chunks
     void* p = nullptr;
-    TLRG_CUDA(cudaMallocAsync(&p, c * sizeof(double), st));
+    if (c == kChunk && ctx_alive(owner)) {
+      std::lock_guard<std::mutex> lk(chunk_mu());
+      auto& v = chunk_cache()[owner];
+      if (!v.empty()) {
+        p = v.back();
+        v.pop_back();
+      }
+    }
+    if (!p) TLRG_CUDA(cudaMallocAsync(&p, c * sizeof(double), st));
     chunks.push_back(p);
+    chunk_len.push_back(c);
     cur = static_cast<double*>(p);
     cap = c;
     used = 0;
@@ -416,7 +463,17 @@ double* Store::alloc(size_t n) {
   return r;
 }
 Store::~Store() {
-  for (void* p : chunks) stream_free(owner, st, p);
+  const bool alive = st && ctx_alive(owner);
+  // chunks go back to the owner's cache once the work touching them is done
+  if (alive && !chunks.empty()) cudaStreamSynchronize(st);
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    if (alive && chunk_len[i] == kChunk) {
+      std::lock_guard<std::mutex> lk(chunk_mu());
+      chunk_cache()[owner].push_back(chunks[i]);
+    } else {
+      stream_free(owner, st, chunks[i]);
+    }
+  }
 }
 
 }  // namespace tlrg

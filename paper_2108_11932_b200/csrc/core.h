@@ -49,12 +49,20 @@ struct DevBuf {
 // exists (Python may collect a matrix after its context); otherwise cudaFree.
 bool ctx_alive(const void* ctx);
 void ctx_register(const void* ctx, bool alive);
+// Per-context cache of standard-size Store chunks: a freed matrix's chunks are
+// reused by the next one without a CUDA call (pool growth under
+// cudaMallocAsync measured 0.5 - 60 ms per 64 MiB chunk inside the loop).
+void chunk_cache_release(const void* ctx);
+// top the cache up to cover `doubles` (one pool call per missing chunk, made
+// while the device is idle at the start of a factorization)
+void chunk_cache_reserve(const void* ctx, size_t doubles, cudaStream_t st);
 void stream_free(const void* ctx, cudaStream_t st, void* p);
 
 struct Store {
   cudaStream_t st = nullptr;  // stream-ordered pool allocations (set by the owner)
   const void* owner = nullptr;
   std::vector<void*> chunks;
+  std::vector<size_t> chunk_len;  // doubles per chunk
   double* cur = nullptr;
   size_t cap = 0, used = 0;
   size_t total = 0;

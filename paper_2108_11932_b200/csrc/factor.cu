@@ -381,6 +381,14 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   store->st = C.st_main;
   store->owner = &C;
   M.stores.push_back(store);
+  {
+    // the factor's panels come from cached chunks: reserve about A's low-rank
+    // footprint (+25 %) now instead of growing the pool inside the column loop
+    size_t lr = 0;
+    for (int i = 1; i < nb; ++i)
+      for (int j = 0; j < i; ++j) lr += (size_t)(M.rows(i) + M.rows(j)) * M.rank[M.t(i, j)];
+    chunk_cache_reserve(&C, lr + lr / 4, C.st_main);
+  }
   double* Dk = C.buf<double>("Dk", (size_t)b * b);
   double* a0 = C.buf<double>("akk0", (size_t)b * b);
   double* aorig = C.buf<double>("akk_orig", (size_t)b * b);

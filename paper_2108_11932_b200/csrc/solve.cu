@@ -466,6 +466,7 @@ double* Ctx::pinned_dbl(size_t n) {
 Ctx::~Ctx() {
   ctx_register(this, false);
   if (st_main) cudaStreamSynchronize(st_main);
+  chunk_cache_release(this);
   if (h_ints) cudaFreeHost(h_ints);
   if (h_dbl) cudaFreeHost(h_dbl);
   bufs.clear();
