@@ -22,6 +22,8 @@
 #include "core.h"
 
 namespace tlrg {
+extern std::chrono::steady_clock::time_point g_col_t0, g_fused_launch;  // factor.cu
+
 
 namespace {
 struct Timer {
@@ -107,7 +109,7 @@ void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int b
 
 void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,
                const std::vector<int>& out_order, ColumnStats& cst, AraOut& out,
-               StreamPrep* pre) {
+               StreamPrep* pre, const std::function<void()>& on_launch) {
   const int T = (int)S.rows.size();
   const int bs = cfg.bs, cols = S.cols;
   const int window = cfg.window > 0 ? cfg.window : bs;
@@ -261,6 +263,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       dprof = C.buf<long long>("fused_prof", (size_t)T * 8);
       fa.prof = dprof;
     }
+    g_fused_launch = std::chrono::steady_clock::now();
     ara_fused(fa, T, maxrows, C.st);
     ++C.launches;
     if (dprof) {
@@ -394,6 +397,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   }
   }
   tm.stop(C.st);
+  if (on_launch) on_launch();
   std::vector<int> hq(T), h_rounds(T), h_conv(T), hact(2);
   std::vector<long long> hav(T), hcur(T);
   TLRG_CUDA(cudaMemcpyAsync(hq.data(), qcols, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));

@@ -9,6 +9,9 @@
 //                  convergence on device, batched exit projection and SVD
 //                  recompression.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -201,7 +204,8 @@ void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPre
 
 std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
                                    const AraCfg& cfg, Store& store, ColumnStats& cst,
-                                   StreamPrep* pre, int part_rank, int part_world) {
+                                   StreamPrep* pre, int part_rank, int part_world,
+                                   const std::function<void()>& on_launch) {
   const int nb = M.nb, b = M.b, rk = M.rows(k), bs = cfg.bs, K = cs.K;
   std::vector<TileResult> res;
   for (int i = k + 1; i < nb; ++i) {
@@ -210,7 +214,15 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
     res.push_back(r);
   }
   if (res.empty()) return res;
+  const char* cpe = std::getenv("TLRG_COLPROF");
+  const bool prof = cpe && cpe[0] == '2';
+  auto tq0 = std::chrono::steady_clock::now();
+  auto since = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0)
+        .count();
+  };
   std::vector<int> queue = column_queue(M, k);
+  const double m_queue = since();
   if (part_world > 1) {
     // intra-column split: slot s of the rank-sorted queue
     // belongs to rank s % world, which balances the fat near-diagonal tiles
@@ -241,9 +253,11 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
     }
     S.Sref.push_back(v);
   }
+  const double m_sref = since();
   const long long Hstride = (long long)b * K;
   double* H = K ? C.buf<double>("H", (size_t)T * Hstride) : nullptr;
   column_H(C, M, cs, queue, H, Hstride);
+  const double m_h = since();
   double* Z = C.buf<double>("Z", (size_t)T * std::max(kAmax, 1) * bs);
   double* T1 = K ? C.buf<double>("T1", (size_t)K * bs * T) : nullptr;
 
@@ -362,7 +376,14 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
   for (int i = k + 1; i < nb; ++i)
     if (slot_of[i] >= 0) out_order.push_back(slot_of[i]);
   AraOut out;
-  ara_batch(C, S, op, cfg, store, out_order, cst, out, pre);
+  const double m_op = since();
+  auto hook = [&] {
+    if (prof)
+      std::fprintf(stderr, "colara %d T=%d J=%zu | queue %.3f sref %.3f H %.3f op %.3f launch %.3f ms\n",
+                   k, T, cs.J.size(), m_queue, m_sref, m_h, m_op, since());
+    if (on_launch) on_launch();
+  };
+  ara_batch(C, S, op, cfg, store, out_order, cst, out, pre, hook);
   for (int i = k + 1; i < nb; ++i) {
     TileResult& r = res[i - k - 1];
     int s = slot_of[i];

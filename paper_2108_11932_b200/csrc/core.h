@@ -302,7 +302,7 @@ void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int b
                      int rounds_ahead, StreamPrep& P);
 void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,
                const std::vector<int>& out_order, ColumnStats& cst, AraOut& out,
-               StreamPrep* pre = nullptr);
+               StreamPrep* pre = nullptr, const std::function<void()>& on_launch = {});
 
 // Dynamic-batched ARA over column k (chol_ara_update, ara.cpp:302-419): all
 // non-trivial tiles resident, converged tiles leave, exit projection and SVD
@@ -311,7 +311,10 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
 std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
                                    const AraCfg& cfg, Store& store, ColumnStats& cst,
                                    StreamPrep* pre = nullptr, int part_rank = 0,
-                                   int part_world = 1);
+                                   int part_world = 1,
+                                   const std::function<void()>& on_launch = {});
+// on_launch: called once the column's ARA work is enqueued (before the host
+// waits on it) -- the factorization enqueues its diagonal path there
 // multi-GPU: replicate the column's new U/V panel (comm.cu)
 void exchange_column(Ctx& C, Comm& cm, const Matrix& M, int k, const std::vector<int>& queue,
                      std::vector<TileResult>& res, double* mine, Store& store);

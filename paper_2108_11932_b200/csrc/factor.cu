@@ -12,6 +12,8 @@
 #include "core.h"
 
 namespace tlrg {
+std::chrono::steady_clock::time_point g_col_t0, g_fused_launch;  // COLPROF probes
+
 
 namespace {
 struct Ev {
@@ -387,7 +389,12 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     size_t lr = 0;
     for (int i = 1; i < nb; ++i)
       for (int j = 0; j < i; ++j) lr += (size_t)(M.rows(i) + M.rows(j)) * M.rank[M.t(i, j)];
+    const auto hr0 = std::chrono::steady_clock::now();
     chunk_cache_reserve(&C, lr + lr / 4, C.st_main);
+    if (std::getenv("TLRG_COLPROF"))
+      std::fprintf(stderr, "factor: reserve %.3f ms host\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hr0)
+                       .count());
   }
   double* Dk = C.buf<double>("Dk", (size_t)b * b);
   double* a0 = C.buf<double>("akk0", (size_t)b * b);
@@ -398,13 +405,23 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   double* piv = C.buf<double>("pivot", (size_t)nb);
   int* info = C.buf<int>("finfo", 4);  // [0] potrf, [1] first singular D block, [2] comp rank, [3] trsm
   int rank_hint = 0;
-  Ev e0, e1, e4, e5, de0, de1, de2, de3, ejoin;
+  Ev e0, e1, e4, e5, de0, de1, de2, de3, ejoin, eprev;
+  double gap_sum = 0, gap_max = 0, gap_first = 0;
+  int gap_arg = -1;
   StreamPrep prep;
 
+  const char* dfe = std::getenv("TLRG_DIAG_FIRST");
+  const bool diag_first = dfe && dfe[0] == '1';
   const char* cpe = std::getenv("TLRG_COLPROF");
   const bool colprof = cpe && cpe[0] == '1';
   for (int k = 0; k < nb; ++k) {
     const auto t_col0 = std::chrono::steady_clock::now();
+    g_col_t0 = t_col0;
+    auto hrel = [&] {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_col0)
+          .count();
+    };
+    double h_setup = 0, h_diag = 0, h_ara = 0;
     const int rk = M.rows(k);
     double* diagk = M.diag + (size_t)k * b * b;
     // ---- gaussian streams of this column's ARA, generated on the side stream
@@ -415,6 +432,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     ColumnSetup cs;
     column_setup(C, M, k, F->D, cs);
     cudaEventRecord(e1.e, C.st);
+    h_setup = hrel();
     const bool comp = opts.schur && k > 0 && cs.K > 0;
     int p_comp = comp ? schur_comp_width(rk, rank_hint) : 0;
 
@@ -454,38 +472,50 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       }
       C.launches += 3;
     };
-    TLRG_CUDA(cudaStreamWaitEvent(C.sd, e1.e, 0));
-    {
-      StreamScope on_diag(C, C.sd);
-      cudaEventRecord(de0.e, C.st);
-      // keep A_kk: the tile is factored in place and a retry re-reads it
-      dcopy(diagk, aorig, (long long)rk * rk, C.st);
-      if (cs.K > 0) {
-        double* Hk = C.buf<double>("Hk", (size_t)b * cs.K);
-        std::vector<int> tk{k};
-        column_H(C, M, cs, tk, Hk, (long long)b * cs.K);
-        std::vector<GemmProblem> pr(1);
-        pr[0] = GemmProblem{};
-        pr[0].A = Hk; pr[0].lda = rk; pr[0].B = cs.Ucat; pr[0].ldb = rk; pr[0].transB = 1;
-        pr[0].C = Dk; pr[0].ldc = rk; pr[0].M = rk; pr[0].N = rk; pr[0].K = cs.K;
-        pr[0].alpha = 1.0;
-        C.gemm(pr);
-        symmetrize(Dk, rk, C.st);
-        ++C.launches;
+    bool diag_enqueued = false;
+    auto enqueue_diag = [&]() {
+      if (diag_enqueued) return;
+      diag_enqueued = true;
+      TLRG_CUDA(cudaStreamWaitEvent(C.sd, e1.e, 0));
+      {
+        StreamScope on_diag(C, C.sd);
+        cudaEventRecord(de0.e, C.st);
+        // keep A_kk: the tile is factored in place and a retry re-reads it
+        dcopy(diagk, aorig, (long long)rk * rk, C.st);
+        if (cs.K > 0) {
+          double* Hk = C.buf<double>("Hk", (size_t)b * cs.K);
+          std::vector<int> tk{k};
+          column_H(C, M, cs, tk, Hk, (long long)b * cs.K);
+          std::vector<GemmProblem> pr(1);
+          pr[0] = GemmProblem{};
+          pr[0].A = Hk; pr[0].lda = rk; pr[0].B = cs.Ucat; pr[0].ldb = rk; pr[0].transB = 1;
+          pr[0].C = Dk; pr[0].ldc = rk; pr[0].M = rk; pr[0].N = rk; pr[0].K = cs.K;
+          pr[0].alpha = 1.0;
+          C.gemm(pr);
+          symmetrize(Dk, rk, C.st);
+          ++C.launches;
+        }
+        cudaEventRecord(de1.e, C.st);
+        if (comp)
+          schur_comp_enqueue(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), p_comp, 0,
+                             corr, frob, info + 2);
+        cudaEventRecord(de2.e, C.st);
+        diag_tail();
+        diag_inverse();
+        cudaEventRecord(de3.e, C.st);
       }
-      cudaEventRecord(de1.e, C.st);
-      if (comp)
-        schur_comp_enqueue(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), p_comp, 0,
-                           corr, frob, info + 2);
-      cudaEventRecord(de2.e, C.st);
-      diag_tail();
-      diag_inverse();
-      cudaEventRecord(de3.e, C.st);
-    }
+      h_diag = hrel();
+    };
+    // the column's ARA is the longer branch in most columns: launch it first and
+    // enqueue the diagonal path while it runs (TLRG_DIAG_FIRST=1: old order)
+    if (diag_first) enqueue_diag();
     // ---- ARA over the column (main stream) -------------------------------------
     ColumnStats cst;
     const int prank = C.comm ? C.comm->rank : 0, pworld = C.comm ? C.comm->world : 1;
-    std::vector<TileResult> res = column_ara(C, M, k, cs, cfg, *store, cst, &prep, prank, pworld);
+    std::vector<TileResult> res =
+        column_ara(C, M, k, cs, cfg, *store, cst, &prep, prank, pworld, enqueue_diag);
+    enqueue_diag();  // no-op unless the column had no ARA work
+    h_ara = hrel();
     S.t_sampling += cst.t_sampling;
     S.t_orthog += cst.t_orthog;
     S.t_projection += cst.t_projection;
@@ -574,6 +604,17 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     cudaEventRecord(e5.e, C.st);
     C.sync();
     S.t_misc += elapsed(e4, e5);
+    {
+      // device time between columns (host work between e5 of k-1 and e0 of k)
+      const double g = k == 0 ? elapsed(d0, e0) : elapsed(eprev, e0);
+      if (k == 0) gap_first = g;
+      else gap_sum += g;
+      if (k > 0 && g > gap_max) {
+        gap_max = g;
+        gap_arg = k;
+      }
+      cudaEventRecord(eprev.e, C.st);
+    }
     if (colprof) {
       auto ms = [](Ev& a, Ev& b) {
         float f = 0;
@@ -584,15 +625,22 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
                                                                t_col0).count();
       std::fprintf(stderr,
                    "col %d T=%zu K=%d | setup %.3f diag %.3f (syrk %.3f comp %.3f fact %.3f) | "
-                   "ara %.3f proj %.3f recomp %.3f | join->end %.3f | dev %.3f host %.3f ms\n",
+                   "ara %.3f proj %.3f recomp %.3f | join->end %.3f | dev %.3f host %.3f ms | "
+                   "host marks: setup %.3f diag %.3f fused-launch %.3f ara-ret %.3f\n",
                    k, res.size(), cs.K, ms(e0, e1), ms(de0, de3), ms(de0, de1), ms(de1, de2),
                    ms(de2, de3), cst.t_sampling * 1e3, cst.t_projection * 1e3,
-                   cst.t_recompress * 1e3, ms(e4, e5), ms(e0, e5), wall_ms);
+                   cst.t_recompress * 1e3, ms(e4, e5), ms(e0, e5), wall_ms, h_setup, h_diag,
+                   std::chrono::duration<double, std::milli>(g_fused_launch - t_col0).count(),
+                   h_ara);
     }
   }
   cudaEventRecord(d1.e, C.st);
   C.sync();
   S.t_device = elapsed(d0, d1);
+  if (colprof)
+    std::fprintf(stderr, "factor: start->col0 %.3f ms, between columns %.3f ms (max %.3f at %d), "
+                 "last->end %.3f ms, total %.3f ms\n", gap_first * 1e3, gap_sum * 1e3,
+                 gap_max * 1e3, gap_arg, elapsed(eprev, d1) * 1e3, S.t_device * 1e3);
   S.kt_gemm_seconds = C.kt_seconds;
   S.kt_gemm_flops = C.kt_flops;
   S.kt_gemm_launches = C.kt_launches;

@@ -366,7 +366,13 @@ class TlrFactor:
         self.h = handle
         self.ctx = ctx
         self.mode = ctx.lib.tlrg_factor_mode(handle)
-        self.L = TlrMatrix(ctx.lib.tlrg_factor_L(handle), ctx, owner=self)
+
+    @property
+    def L(self) -> TlrMatrix:
+        # a fresh view each time: the view keeps the factor alive, the factor
+        # holds no reference back (no cycle, so `del F` frees the device memory
+        # at once instead of at the next cyclic GC pass)
+        return TlrMatrix(self.ctx.lib.tlrg_factor_L(self.h), self.ctx, owner=self)
 
     def __del__(self):
         if getattr(self, "h", None) is not None:
