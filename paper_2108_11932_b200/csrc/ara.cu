@@ -22,7 +22,8 @@
 #include "core.h"
 
 namespace tlrg {
-extern std::chrono::steady_clock::time_point g_col_t0, g_fused_launch;  // factor.cu
+extern std::chrono::steady_clock::time_point g_col_t0, g_fused_launch, g_ara_waited,
+    g_ara_recomp;  // factor.cu (COLPROF probes)
 
 
 namespace {
@@ -415,6 +416,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     TLRG_CUDA(cudaMemcpyAsync(h_fl.data(), fl_dev, sizeof(double) * T, cudaMemcpyDeviceToHost,
                               C.st));
   C.wait();
+  g_ara_waited = std::chrono::steady_clock::now();
   for (auto& gc : graph_cleanup) {
     cudaGraphExecDestroy(gc.first);
     cudaGraphDestroy(gc.second);
@@ -574,6 +576,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   if (recomp_in_kernel)
     for (int s = 0; s < T; ++s)
       if (h_rank_in[s] >= 0) fr[s] = h_rank_in[s];
+  g_ara_recomp = std::chrono::steady_clock::now();
   // ---- final factors into one contiguous panel (in out_order) -------------
   long long utot = 0, vtot = 0;
   for (int s : out_order) {

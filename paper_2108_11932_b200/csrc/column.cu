@@ -162,6 +162,36 @@ void column_H(Ctx& C, const Matrix& M, const ColumnSetup& cs, const std::vector<
   ++C.launches;
 }
 
+// column_H with the T x J block list expanded on the device (tile-table mirror)
+static void column_H_dev(Ctx& C, const Matrix& M, const ColumnSetup& cs,
+                         const std::vector<int>& targets, double* H, long long stride) {
+  if (cs.K == 0 || targets.empty() || cs.J.empty()) return;
+  const int T = (int)targets.size(), nJ = (int)cs.J.size();
+  std::vector<long long> cols((size_t)T + 5 * nJ);
+  for (int t = 0; t < T; ++t) cols[t] = targets[t];
+  for (int jj = 0; jj < nJ; ++jj) {
+    cols[T + jj] = cs.J[jj];
+    cols[T + nJ + jj] = cs.S[jj];
+    cols[T + 2 * nJ + jj] = cs.seg[jj];
+    cols[T + 3 * nJ + jj] = M.rank[M.t(cs.k, cs.J[jj])];
+    cols[T + 4 * nJ + jj] = cs.goff[jj];
+  }
+  HProductArgs a{};
+  a.cols = C.push(cols);
+  a.rank = cs.d_rank;
+  a.U = cs.d_U;
+  a.G = cs.G;
+  a.H = H;
+  a.stride = stride;
+  a.n = M.n;
+  a.T = T;
+  a.nJ = nJ;
+  a.k = cs.k;
+  a.b = M.b;
+  h_products(a, C.st);
+  ++C.launches;
+}
+
 std::vector<int> column_queue(const Matrix& M, int k) {
   std::vector<int> order;
   for (int i = k + 1; i < M.nb; ++i) order.push_back(i);
@@ -256,7 +286,8 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
   const double m_sref = since();
   const long long Hstride = (long long)b * K;
   double* H = K ? C.buf<double>("H", (size_t)T * Hstride) : nullptr;
-  column_H(C, M, cs, queue, H, Hstride);
+  if (cs.d_rank) column_H_dev(C, M, cs, queue, H, Hstride);
+  else column_H(C, M, cs, queue, H, Hstride);
   const double m_h = since();
   double* Z = C.buf<double>("Z", (size_t)T * std::max(kAmax, 1) * bs);
   double* T1 = K ? C.buf<double>("T1", (size_t)K * bs * T) : nullptr;

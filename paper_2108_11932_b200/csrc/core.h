@@ -246,6 +246,10 @@ struct ColumnSetup {
   std::vector<long long> goff; // per J entry
   std::vector<int> S;          // per J entry
   std::vector<int> sub_first;  // first i of the gathered suffix (k)
+  // device mirror of the tile tables (set by the factorization): the ARA's
+  // H_i products then derive their block fields on the device
+  const int* d_rank = nullptr;
+  const double* const* d_U = nullptr;
 };
 
 void column_setup(Ctx& C, const Matrix& M, int k, const DBlocks& D, ColumnSetup& cs);

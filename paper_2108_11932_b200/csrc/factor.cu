@@ -12,7 +12,8 @@
 #include "core.h"
 
 namespace tlrg {
-std::chrono::steady_clock::time_point g_col_t0, g_fused_launch;  // COLPROF probes
+std::chrono::steady_clock::time_point g_col_t0, g_fused_launch, g_ara_waited,
+    g_ara_recomp;  // COLPROF probes
 
 
 namespace {
@@ -396,6 +397,22 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hr0)
                        .count());
   }
+  // device mirror of the tile tables (rank, U pointer per lower tile), kept
+  // current column by column: the ARA's H_i block list is derived on the device
+  const long long ntri = (long long)nb * (nb - 1) / 2;
+  int* d_rank = nullptr;
+  const double** d_U = nullptr;
+  {
+    const char* hh = std::getenv("TLRG_HOST_H");
+    if (ntri > 0 && !(hh && hh[0] == '1')) {
+      d_rank = C.buf<int>("tri_rank", (size_t)ntri);
+      d_U = reinterpret_cast<const double**>(C.buf<uintptr_t>("tri_U", (size_t)ntri));
+      TLRG_CUDA(cudaMemcpyAsync(d_rank, M.rank.data(), sizeof(int) * ntri, cudaMemcpyHostToDevice,
+                                C.st));
+      TLRG_CUDA(cudaMemcpyAsync(d_U, M.U.data(), sizeof(double*) * ntri, cudaMemcpyHostToDevice,
+                                C.st));
+    }
+  }
   double* Dk = C.buf<double>("Dk", (size_t)b * b);
   double* a0 = C.buf<double>("akk0", (size_t)b * b);
   double* aorig = C.buf<double>("akk_orig", (size_t)b * b);
@@ -431,6 +448,8 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     cudaEventRecord(e0.e, C.st);
     ColumnSetup cs;
     column_setup(C, M, k, F->D, cs);
+    cs.d_rank = d_rank;
+    cs.d_U = d_U;
     cudaEventRecord(e1.e, C.st);
     h_setup = hrel();
     const bool comp = opts.schur && k > 0 && cs.K > 0;
@@ -601,6 +620,18 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       M.U[t] = r.U;
       M.V[t] = r.V;
     }
+    if (d_rank && !res.empty()) {
+      std::vector<long long> ut;
+      std::vector<int> ur;
+      std::vector<const double*> uu;
+      for (auto& r : res) {
+        ut.push_back(M.t(r.i, k));
+        ur.push_back(r.rank);
+        uu.push_back(r.U);
+      }
+      tri_update(C.push(ut), C.push(ur), C.push(uu), (int)res.size(), d_rank, d_U, C.st);
+      ++C.launches;
+    }
     cudaEventRecord(e5.e, C.st);
     C.sync();
     S.t_misc += elapsed(e4, e5);
@@ -626,11 +657,14 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       std::fprintf(stderr,
                    "col %d T=%zu K=%d | setup %.3f diag %.3f (syrk %.3f comp %.3f fact %.3f) | "
                    "ara %.3f proj %.3f recomp %.3f | join->end %.3f | dev %.3f host %.3f ms | "
-                   "host marks: setup %.3f diag %.3f fused-launch %.3f ara-ret %.3f\n",
+                   "host marks: setup %.3f diag %.3f fused-launch %.3f waited %.3f recomp-done %.3f "
+                   "ara-ret %.3f\n",
                    k, res.size(), cs.K, ms(e0, e1), ms(de0, de3), ms(de0, de1), ms(de1, de2),
                    ms(de2, de3), cst.t_sampling * 1e3, cst.t_projection * 1e3,
                    cst.t_recompress * 1e3, ms(e4, e5), ms(e0, e5), wall_ms, h_setup, h_diag,
                    std::chrono::duration<double, std::milli>(g_fused_launch - t_col0).count(),
+                   std::chrono::duration<double, std::milli>(g_ara_waited - t_col0).count(),
+                   std::chrono::duration<double, std::milli>(g_ara_recomp - t_col0).count(),
                    h_ara);
     }
   }

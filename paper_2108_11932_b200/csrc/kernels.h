@@ -157,6 +157,23 @@ struct BlockItem {
   int rows, kij, kkj;
 };
 void block_products(BlockItem* d_items, int nitems, int max_rows, cudaStream_t st);
+// The same products with the per-block fields derived on the device from the
+// tile tables (rank / U pointer per lower tile, tri_index order) instead of a
+// host-expanded T x J item list.  cols: [targets T | J nJ | S nJ | seg nJ |
+// kkj nJ | goff nJ].  Block (t, jj) = blockIdx.x = t * nJ + jj.
+struct HProductArgs {
+  const long long* cols;
+  const int* rank;
+  const double* const* U;
+  const double* G;
+  double* H;
+  long long stride, n;
+  int T, nJ, k, b;
+};
+void h_products(const HProductArgs& a, cudaStream_t st);
+// tile-table mirror update: rank[t[e]] = r[e], U[t[e]] = u[e]
+void tri_update(const long long* t, const int* r, const double* const* u, int n, int* rank,
+                const double** U, cudaStream_t st);
 
 // Copy/gather helpers
 struct CopyItem {

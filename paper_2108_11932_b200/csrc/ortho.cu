@@ -458,6 +458,58 @@ void block_products(BlockItem* d_items, int nitems, int, cudaStream_t st) {
   TLRG_CUDA(cudaGetLastError());
 }
 
+__global__ void __launch_bounds__(128) h_products_kernel(HProductArgs a) {
+  const int t = blockIdx.x / a.nJ, jj = blockIdx.x - t * a.nJ;
+  const long long* tg = a.cols;
+  const long long* Jl = tg + a.T;
+  const int i = (int)tg[t], j = (int)Jl[jj];
+  const int rows = (int)min((long long)a.b, a.n - (long long)i * a.b);
+  const long long tij = tri_index(i, j);
+  const int kij = a.rank[tij], kkj = (int)Jl[3 * a.nJ + jj];
+  // row offset of G_ij inside G_j: ranks of rows k .. i-1 in column j
+  __shared__ int s_pre;
+  if (threadIdx.x < 32) {
+    int s = 0;
+    for (int r = a.k + (int)threadIdx.x; r < i; r += 32) s += a.rank[tri_index(r, j)];
+    s = warp_sum_int(s);
+    if (threadIdx.x == 0) s_pre = s;
+  }
+  __syncthreads();
+  const long long ldg = max((long long)Jl[a.nJ + jj], 1LL);
+  const double* U = kij ? a.U[tij] : nullptr;
+  const double* G = a.G + Jl[4 * a.nJ + jj] + s_pre;
+  double* H = a.H + t * a.stride + Jl[2 * a.nJ + jj] * rows;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    for (int c = 0; c < kkj; ++c) {
+      double s = 0.0;
+      for (int p = 0; p < kij; ++p) s += U[(long long)p * rows + r] * G[p + c * ldg];
+      H[r + c * rows] = s;
+    }
+  }
+}
+
+void h_products(const HProductArgs& a, cudaStream_t st) {
+  if (a.T <= 0 || a.nJ <= 0) return;
+  h_products_kernel<<<a.T * a.nJ, 128, 0, st>>>(a);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+__global__ void tri_update_kernel(const long long* t, const int* r, const double* const* u, int n,
+                                  int* rank, const double** U) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) {
+    rank[t[e]] = r[e];
+    U[t[e]] = u[e];
+  }
+}
+
+void tri_update(const long long* t, const int* r, const double* const* u, int n, int* rank,
+                const double** U, cudaStream_t st) {
+  if (n <= 0) return;
+  tri_update_kernel<<<(n + 127) / 128, 128, 0, st>>>(t, r, u, n, rank, U);
+  TLRG_CUDA(cudaGetLastError());
+}
+
 __global__ void batched_copy_kernel(const CopyItem* items) {
   const CopyItem& C = items[blockIdx.x];
   long long n = (long long)C.rows * C.cols;
