@@ -17,6 +17,8 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <map>
 #include <numeric>
 
 #include "core.h"
@@ -27,12 +29,28 @@ extern std::chrono::steady_clock::time_point g_col_t0, g_fused_launch, g_ara_wai
 
 
 namespace {
+// CUDA events recycled per thread and device (creating and destroying six
+// events per column cost tens of microseconds of host time in the loop)
+std::vector<cudaEvent_t>& event_pool() {
+  thread_local std::map<int, std::vector<cudaEvent_t>> pools;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return pools[dev];
+}
+cudaEvent_t event_take() {
+  auto& p = event_pool();
+  if (p.empty()) {
+    cudaEvent_t e;
+    TLRG_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = p.back();
+  p.pop_back();
+  return e;
+}
 struct Timer {
   cudaEvent_t a, b;
-  explicit Timer() {
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-  }
+  explicit Timer() : a(event_take()), b(event_take()) {}
   void start(cudaStream_t s) { cudaEventRecord(a, s); }
   void stop(cudaStream_t s) { cudaEventRecord(b, s); }
   double sec() {
@@ -42,8 +60,9 @@ struct Timer {
     return f * 1e-3;
   }
   ~Timer() {
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    auto& p = event_pool();
+    p.push_back(a);
+    p.push_back(b);
   }
 };
 __global__ void ara_loop_cond_kernel(cudaGraphConditionalHandle h, int* active, int max_rounds) {
@@ -401,21 +420,38 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   if (on_launch) on_launch();
   std::vector<int> hq(T), h_rounds(T), h_conv(T), hact(2);
   std::vector<long long> hav(T), hcur(T);
-  TLRG_CUDA(cudaMemcpyAsync(hq.data(), qcols, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
-  TLRG_CUDA(cudaMemcpyAsync(h_rounds.data(), rounds, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
-  TLRG_CUDA(cudaMemcpyAsync(h_conv.data(), conv, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
-  TLRG_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * 2, cudaMemcpyDeviceToHost, C.st));
-  TLRG_CUDA(cudaMemcpyAsync(hav.data(), G.avail, sizeof(long long) * T, cudaMemcpyDeviceToHost,
-                            C.st));
-  TLRG_CUDA(cudaMemcpyAsync(hcur.data(), G.cursor, sizeof(long long) * T, cudaMemcpyDeviceToHost,
-                            C.st));
-  if (recomp_in_kernel)
-    TLRG_CUDA(cudaMemcpyAsync(h_rank_in.data(), rank_in, sizeof(int) * T, cudaMemcpyDeviceToHost,
-                              C.st));
-  if (fl_dev)
-    TLRG_CUDA(cudaMemcpyAsync(h_fl.data(), fl_dev, sizeof(double) * T, cudaMemcpyDeviceToHost,
-                              C.st));
-  C.wait();
+  {
+    // all per-tile results in a few copies into pinned staging (pageable
+    // destinations would make every copy its own blocking round trip)
+    int* hI = C.pinned_ints((size_t)4 * T + 2);  // [q | rounds | conv | rank_in | active]
+    double* hD = C.pinned_dbl((size_t)3 * T);   // [avail | cursor | flops]
+    TLRG_CUDA(cudaMemcpyAsync(hI, qcols, sizeof(int) * 3 * T, cudaMemcpyDeviceToHost, C.st));
+    if (recomp_in_kernel)
+      TLRG_CUDA(cudaMemcpyAsync(hI + 3 * T, rank_in, sizeof(int) * T, cudaMemcpyDeviceToHost,
+                                C.st));
+    TLRG_CUDA(cudaMemcpyAsync(hI + 4 * T, active, sizeof(int) * 2, cudaMemcpyDeviceToHost, C.st));
+    if (G.cursor == G.avail + T) {
+      TLRG_CUDA(cudaMemcpyAsync(hD, G.avail, sizeof(long long) * 2 * T, cudaMemcpyDeviceToHost,
+                                C.st));
+    } else {
+      TLRG_CUDA(cudaMemcpyAsync(hD, G.avail, sizeof(long long) * T, cudaMemcpyDeviceToHost, C.st));
+      TLRG_CUDA(cudaMemcpyAsync(hD + T, G.cursor, sizeof(long long) * T, cudaMemcpyDeviceToHost,
+                                C.st));
+    }
+    if (fl_dev)
+      TLRG_CUDA(cudaMemcpyAsync(hD + 2 * T, fl_dev, sizeof(double) * T, cudaMemcpyDeviceToHost,
+                                C.st));
+    C.wait();
+    std::copy(hI, hI + T, hq.begin());
+    std::copy(hI + T, hI + 2 * T, h_rounds.begin());
+    std::copy(hI + 2 * T, hI + 3 * T, h_conv.begin());
+    if (recomp_in_kernel) std::copy(hI + 3 * T, hI + 4 * T, h_rank_in.begin());
+    hact[0] = hI[4 * T];
+    hact[1] = hI[4 * T + 1];
+    std::memcpy(hav.data(), hD, sizeof(long long) * T);
+    std::memcpy(hcur.data(), hD + T, sizeof(long long) * T);
+    if (fl_dev) std::copy(hD + 2 * T, hD + 3 * T, h_fl.begin());
+  }
   g_ara_waited = std::chrono::steady_clock::now();
   for (auto& gc : graph_cleanup) {
     cudaGraphExecDestroy(gc.first);
