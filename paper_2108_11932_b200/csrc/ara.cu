@@ -203,7 +203,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   std::vector<int> q(T, 0);
   int* active = C.buf<int>("active", 2);  // [0] tiles still resident, [1] loop counter
   int* d_rows = C.buf<int>("slot_rows", (size_t)T);
-  {
+  if (!use_fused) {  // round-loop state of the graph path
     std::vector<int> init{T, 0};
     TLRG_CUDA(cudaMemcpyAsync(active, init.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, C.st));
     TLRG_CUDA(cudaMemcpyAsync(d_rows, S.rows.data(), sizeof(int) * T, cudaMemcpyHostToDevice,
@@ -429,7 +429,9 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     if (recomp_in_kernel)
       TLRG_CUDA(cudaMemcpyAsync(hI + 3 * T, rank_in, sizeof(int) * T, cudaMemcpyDeviceToHost,
                                 C.st));
-    TLRG_CUDA(cudaMemcpyAsync(hI + 4 * T, active, sizeof(int) * 2, cudaMemcpyDeviceToHost, C.st));
+    if (!use_fused)
+      TLRG_CUDA(cudaMemcpyAsync(hI + 4 * T, active, sizeof(int) * 2, cudaMemcpyDeviceToHost,
+                                C.st));
     if (G.cursor == G.avail + T) {
       TLRG_CUDA(cudaMemcpyAsync(hD, G.avail, sizeof(long long) * 2 * T, cudaMemcpyDeviceToHost,
                                 C.st));
