@@ -102,6 +102,19 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(path=os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                  "r01h_fused_ncu.txt")):
+    """DRAM bytes of one fused-kernel launch from the committed ncu capture."""
+    try:
+        tot = 0
+        for line in open(path):
+            if line.startswith(("dram__bytes_read.sum:", "dram__bytes_write.sum:")):
+                tot += int(float(line.split(":")[1].split()[0]))
+        return tot or None
+    except OSError:
+        return None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -354,7 +367,10 @@ def run_tlrg(args):
                                     "has no FP64 entry)",
                      "frac": round(st.flops_ara_kernel / st.t_ara_kernel / 1e12 / peak, 5)
                      if st.t_ara_kernel and peak else None,
-                     "traffic": None,
+                     "traffic": ncu_traffic(),
+                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                       "ara_fused_kernel launch (cfg2 column 110), "
+                                       "profiles/r01h_fused_ncu.txt",
                      "kernel_share_of_step": round(st.t_ara_kernel / st.t_device, 4)
                      if st.t_device else None,
                      "algorithmic_flops_per_factorization": st.flops_ara_kernel,
