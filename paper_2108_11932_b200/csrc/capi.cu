@@ -286,7 +286,15 @@ int tlrg_create(int device, tlrg_ctx* out, tlrg_status* st) {
     c->c.device = device;
     TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.st, cudaStreamNonBlocking));
     TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.st2, cudaStreamNonBlocking));
-    TLRG_CUDA(cudaStreamCreateWithFlags(&c->c.sd, cudaStreamNonBlocking));
+    {
+      // the diagonal path's few-CTA kernels run beside the column's one-CTA-per-
+      // tile ARA: high priority lets them take SMs ahead of the ARA's second wave
+      int lo = 0, hi = 0;
+      TLRG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const char* pe = std::getenv("TLRG_SD_PRIO");
+      const bool prio = !(pe && pe[0] == '0');
+      TLRG_CUDA(cudaStreamCreateWithPriority(&c->c.sd, cudaStreamNonBlocking, prio ? hi : lo));
+    }
     c->c.st_main = c->c.st;
     ctx_register(&c->c, true);
     {
