@@ -123,3 +123,28 @@ def test_device_build_matches_reference_build(tg, ref, kind, n, b, eps, kernel, 
         assert np.abs(x - y).max() <= 1e-15
     for u1, v1, u2, v2 in zip(U1, V1, U2, V2):
         assert np.abs(u1 @ v1.T - u2 @ v2.T).max() <= 2 * eps
+
+
+def test_factor_is_freed_at_del_and_repeat_factorizations_are_identical(tg, ref):
+    """A factor owns its panels until `del` (no reference cycle through F.L), and
+    panel chunks recycled through the context cache give bitwise-identical
+    factors on repeated runs."""
+    import weakref
+
+    eps = 1e-6
+    A_ref = covariance_ref(ref, 1024, 128, eps, seed=42)
+    A = to_gpu(tg, A_ref)
+    outs = []
+    for _ in range(3):
+        F = tg.tlr_cholesky(A.copy(), _cfg(tg, eps))
+        L = F.L
+        Ld, r, U, V = L.to_parts()
+        outs.append((np.concatenate([d.ravel() for d in Ld]), r.copy(),
+                     np.concatenate([u.ravel() for u in U if u.size] or [np.zeros(0)]),
+                     np.concatenate([v.ravel() for v in V if v.size] or [np.zeros(0)])))
+        w = weakref.ref(F)
+        del F, L
+        assert w() is None
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
