@@ -666,6 +666,10 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     ++C.launches;
   }
   tr.stop(C.st);
+  // with every tile finished in the fused kernel the projection/recompression
+  // phases are empty: leave the panel copy in flight (the column's join waits
+  // on this stream) instead of a host round trip just to read the timers
+  if (use_fused && qmax == 0) return;
   C.wait();
   if (recprof && qmax > 0) {
     int nf = 0;
