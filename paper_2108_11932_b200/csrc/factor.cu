@@ -543,12 +543,45 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     S.t_fused += cst.t_fused;
     S.flops_fused += cst.flops_fused;
     S.fused_launches += cst.fused_launches;
-    // ---- join: diagonal status (one small read) ---------------------------------
+    // ---- join: diagonal status (one small read, after the TRSM is enqueued) ----
     TLRG_CUDA(cudaStreamWaitEvent(C.st, de3.e, 0));
     int* hs = C.pinned_ints(4);
     double* hf = C.pinned_dbl(1);
     TLRG_CUDA(cudaMemcpyAsync(hs, info, sizeof(int) * 4, cudaMemcpyDeviceToHost, C.st));
     if (comp) TLRG_CUDA(cudaMemcpyAsync(hf, frob, sizeof(double), cudaMemcpyDeviceToHost, C.st));
+    // ---- TRSM of the new panel (one GEMM with the precomputed operator),
+    //      enqueued before the status read: the rare retry / fallback below
+    //      recomputes the operator and re-runs the GEMM from the saved copy Bs
+    cudaEventRecord(e4.e, C.st);
+    double* Vp = nullptr;
+    double* Up0 = nullptr;
+    double* Bs = nullptr;
+    long long ncols = 0;
+    for (auto& r : res) {
+      if (r.rank > 0 && !Vp) {
+        Vp = r.V;
+        Up0 = r.U;
+      }
+      ncols += r.rank;  // this rank's tiles only (the others are still empty)
+      S.ara_rounds[k] += r.rounds;
+    }
+    S.tile_rounds_resident += S.ara_rounds[k];
+    auto trsm_gemm = [&]() {
+      std::vector<GemmProblem> pr(1);
+      pr[0] = GemmProblem{};
+      pr[0].A = Xinv; pr[0].lda = rk; pr[0].B = Bs; pr[0].ldb = rk;
+      pr[0].C = Vp; pr[0].ldc = rk; pr[0].M = rk; pr[0].N = (int)ncols; pr[0].K = rk;
+      pr[0].alpha = 1.0;
+      C.gemm(pr);
+      ++C.launches;
+    };
+    if (ncols > 0) {
+      Bs = C.buf<double>("trsm_B", (size_t)rk * ncols);
+      TLRG_CUDA(cudaMemcpyAsync(Bs, Vp, sizeof(double) * rk * ncols, cudaMemcpyDeviceToDevice,
+                                C.st));
+      trsm_gemm();
+    }
+    bool redo_trsm = false;
     C.wait();
     int st_potrf = hs[0], st_sing = hs[1], st_rank = hs[2];
     if (comp && st_rank > p_comp - 8 && p_comp < std::min(rk, kSchurMaxWidth)) {
@@ -563,6 +596,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       st_potrf = hs[0];
       st_sing = hs[1];
       diag_inverse();
+      redo_trsm = true;
     } else if (comp) {
       rank_hint = st_rank;
     }
@@ -574,7 +608,9 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       modified_cholesky_device(C, diagk, rk);
       S.modified_diagonals++;
       diag_inverse();
+      redo_trsm = true;
     }
+    if (redo_trsm && ncols > 0) trsm_gemm();
     {
       float f = 0;
       cudaEventElapsedTime(&f, e0.e, e1.e);
@@ -586,32 +622,6 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       S.t_misc += f * 1e-3;
       cudaEventElapsedTime(&f, de2.e, de3.e);
       S.t_misc += f * 1e-3;
-    }
-    // ---- TRSM of the new panel (one GEMM with the precomputed operator) --------
-    cudaEventRecord(e4.e, C.st);
-    double* Vp = nullptr;
-    double* Up0 = nullptr;
-    long long ncols = 0;
-    for (auto& r : res) {
-      if (r.rank > 0 && !Vp) {
-        Vp = r.V;
-        Up0 = r.U;
-      }
-      ncols += r.rank;  // this rank's tiles only (the others are still empty)
-      S.ara_rounds[k] += r.rounds;
-    }
-    S.tile_rounds_resident += S.ara_rounds[k];
-    if (ncols > 0) {
-      double* Bs = C.buf<double>("trsm_B", (size_t)rk * ncols);
-      TLRG_CUDA(cudaMemcpyAsync(Bs, Vp, sizeof(double) * rk * ncols, cudaMemcpyDeviceToDevice,
-                                C.st));
-      std::vector<GemmProblem> pr(1);
-      pr[0] = GemmProblem{};
-      pr[0].A = Xinv; pr[0].lda = rk; pr[0].B = Bs; pr[0].ldb = rk;
-      pr[0].C = Vp; pr[0].ldc = rk; pr[0].M = rk; pr[0].N = (int)ncols; pr[0].K = rk;
-      pr[0].alpha = 1.0;
-      C.gemm(pr);
-      ++C.launches;
     }
     if (pworld > 1) exchange_column(C, *C.comm, M, k, column_queue(M, k), res, Up0, *store);
     for (auto& r : res) {
