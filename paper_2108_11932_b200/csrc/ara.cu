@@ -24,7 +24,7 @@
 #include "core.h"
 
 namespace tlrg {
-extern std::chrono::steady_clock::time_point g_col_t0, g_fused_launch, g_ara_waited,
+extern std::chrono::steady_clock::time_point g_fused_launch, g_ara_waited,
     g_ara_recomp;  // factor.cu (COLPROF probes)
 
 
@@ -108,7 +108,6 @@ void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int b
   G.avail = gl;
   G.cursor = gl + T;
   P.pre = std::min<long long>(G.cap, (long long)rounds_ahead * cols * bs + 2LL * bs * maxrows);
-  (void)0;
   P.pre &= ~1LL;
   uint64_t* d_seeds = C.buf<uint64_t>("p_seeds", (size_t)T);
   int* d_slots = C.buf<int>("p_slots", (size_t)T);
@@ -198,7 +197,6 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       ++C.launches;
     }
   };
-  int h_flags_unused = 0;
 
   std::vector<int> q(T, 0);
   int* active = C.buf<int>("active", 2);  // [0] tiles still resident, [1] loop counter
@@ -472,7 +470,6 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     cst.t_fused += tm.sec();
     cst.fused_launches += 1;
     for (int s = 0; s < T; ++s) cst.flops_fused += h_fl[s];
-    C.flops += 0.0;
   }
   for (int s = 0; s < T; ++s) {
     q[s] = hq[s];
@@ -481,7 +478,6 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     cst.tile_rounds += h_rounds[s];
     if (!S.Sref.empty()) cst.flops_ref += (double)bs * h_rounds[s] * S.Sref[s];
   }
-  (void)h_flags_unused;
   {
     const char* fp = std::getenv("TLRG_FUSED_PROF");
     if (fp && fp[0] == '1') {

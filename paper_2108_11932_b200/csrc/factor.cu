@@ -12,8 +12,8 @@
 #include "core.h"
 
 namespace tlrg {
-std::chrono::steady_clock::time_point g_col_t0, g_fused_launch, g_ara_waited,
-    g_ara_recomp;  // COLPROF probes
+std::chrono::steady_clock::time_point g_fused_launch, g_ara_waited,
+    g_ara_recomp;  // COLPROF probes (set in ara.cu)
 
 
 namespace {
@@ -433,7 +433,6 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   const bool colprof = cpe && cpe[0] == '1';
   for (int k = 0; k < nb; ++k) {
     const auto t_col0 = std::chrono::steady_clock::now();
-    g_col_t0 = t_col0;
     auto hrel = [&] {
       return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_col0)
           .count();
