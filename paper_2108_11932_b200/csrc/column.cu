@@ -213,8 +213,15 @@ std::vector<int> column_queue(const Matrix& M, int k) {
 }
 
 void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPrep& P) {
-  std::vector<int> queue = column_queue(M, k);
   P.T = 0;
+  {
+    // the fused ARA needs no pre-generated streams; eligibility of all rows
+    // i > k implies it for the queue (a subset), without building the queue
+    std::vector<int> rws;
+    for (int i = k + 1; i < M.nb; ++i) rws.push_back(M.rows(i));
+    if (ara_fused_eligible(M.rows(k), rws, cfg.bs, cfg.window > 0 ? cfg.window : cfg.bs)) return;
+  }
+  std::vector<int> queue = column_queue(M, k);
   {
     std::vector<int> rws;
     for (int i : queue) rws.push_back(M.rows(i));
