@@ -282,14 +282,21 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
     S.seeds.push_back(ara_column_seed(cfg.seed, i, k));
     kA[s] = M.rank[M.t(i, k)];
     kAmax = std::max(kAmax, kA[s]);
-    // reference-formulation flops per sampled vector
-    double v = 4.0 * rk * kA[s];
-    for (int j = 0; j < k; ++j) {
-      int a = M.rank[M.t(k, j)], c = M.rank[M.t(i, j)];
-      if (a > 0 && c > 0) v += 4.0 * b * (a + c);
-    }
-    S.Sref.push_back(v);
   }
+  // reference-formulation flops per sampled vector; statistics
+  // only, read by ara_batch after the kernel: filled while the ARA runs
+  auto fill_sref = [&]() {
+    S.Sref.resize(T);
+    for (int s = 0; s < T; ++s) {
+      const int i = queue[s];
+      double v = 4.0 * rk * kA[s];
+      for (int j = 0; j < k; ++j) {
+        int a = M.rank[M.t(k, j)], c = M.rank[M.t(i, j)];
+        if (a > 0 && c > 0) v += 4.0 * b * (a + c);
+      }
+      S.Sref[s] = v;
+    }
+  };
   const double m_sref = since();
   const long long Hstride = (long long)b * K;
   double* H = K ? C.buf<double>("H", (size_t)T * Hstride) : nullptr;
@@ -420,6 +427,7 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
       std::fprintf(stderr, "colara %d T=%d J=%zu | queue %.3f sref %.3f H %.3f op %.3f launch %.3f ms\n",
                    k, T, cs.J.size(), m_queue, m_sref, m_h, m_op, since());
     if (on_launch) on_launch();
+    fill_sref();
   };
   ara_batch(C, S, op, cfg, store, out_order, cst, out, pre, hook);
   for (int i = k + 1; i < nb; ++i) {
