@@ -139,7 +139,8 @@ tlrg_matrix tlrg_factor_L(tlrg_factor f);
 int tlrg_factor_mode(tlrg_factor f);
 int tlrg_factor_stats(tlrg_factor f, tlrg_stats* out, int32_t* ara_rounds /* nb */,
                       double* pivot_trace /* nb */);
-/* LDL^T parts of column k: d[n], e[n-1], start2x2[n], intra_perm[n] */
+/* LDL^T parts of column k: d[n], e[n-1], start2x2[n], intra_perm[n].
+   Returns 0, 2 (Cholesky factor or k out of range) or 1 (copy failed). */
 int tlrg_factor_dblock(tlrg_factor f, int32_t k, double* d, double* e, uint8_t* s2, int32_t* perm);
 /* TLRF I/O (factor.cpp:308-395) */
 int tlrg_write_factor(tlrg_factor f, const char* path, tlrg_status* st);
@@ -154,6 +155,16 @@ int tlrg_tlr_matvec(tlrg_matrix A, const double* x, double* y, tlrg_status* st);
 int tlrg_estimate_2norm_diff(tlrg_matrix A, tlrg_factor f, int32_t iters, uint64_t seed,
                              double* out, tlrg_status* st);
 int tlrg_estimate_2norm(tlrg_matrix A, int32_t iters, uint64_t seed, double* out, tlrg_status* st);
+/* Accuracy gates of the north star (no reference
+ * function, the oracle restates the identical estimator in
+ * oracle/ref_capi.cpp ref_estimate_frob_diff):
+ *   tlrg_frob_norm          ||A||_F exact tile-wise
+ *   tlrg_estimate_frob_diff Hutchinson estimate of ||P A P^T - L L^T||_F with
+ *                           `probes` gaussian probes g_t = tlr::Rng(tile_seed(seed,
+ *                           0xF20B, t, 0)), E g_t as difference_apply (solve.cpp:283-297) */
+int tlrg_frob_norm(tlrg_matrix A, double* out, tlrg_status* st);
+int tlrg_estimate_frob_diff(tlrg_matrix A, tlrg_factor f, int32_t probes, uint64_t seed,
+                            double* out, tlrg_status* st);
 
 /* ------------------------------------------------- building blocks (tests) -- */
 /* sample_left / sample_left_transpose (ara.cpp:275-300).  omegas: per row tile,
@@ -173,6 +184,9 @@ int tlrg_ara_count(tlrg_ara a);
 /* info[4] = i, rank, converged, rounds; Q rows(i) x rank, B rows(k) x rank */
 int tlrg_ara_tile(tlrg_ara a, int32_t t, int32_t* info, double* Q, double* B);
 void tlrg_ara_free(tlrg_ara a);
+/* timing of the last tlrg_chol_ara_update: [t_device s, tile-rounds,
+ * reference-formulation flops, fused-kernel s, fused-kernel flops] */
+void tlrg_ara_stats(tlrg_ara a, double* out5);
 /* first n gaussians of tlr::Rng(seed) generated on the device */
 int tlrg_rng_gaussians(tlrg_ctx ctx, uint64_t seed, int64_t n, double* out, tlrg_status* st);
 /* orthog (dense_kernels.cpp:379-420) on the device; same outputs as the

@@ -4,6 +4,7 @@
 #include "tlr_b200.hpp"
 
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -129,13 +130,13 @@ TlrFactor run(TlrMatrix A, const AraConfig& c, const AraWorkspace& w, const Fact
                       c.recompress ? 1 : 0, c.seed};
   tlrg_workspace ws{w.parallel_buffers, w.dense_buffers, w.subset_capacity};
   tlrg_factor_options fo{o.schur_compensation ? 1 : 0, o.diag_shift};
-  tlrg_matrix h = upload(A);  // consumed by tlrg_factorize
+  tlrg_matrix h = upload(A);  // consumed by tlrg_factorize (even when it fails)
   tlrg_factor f = nullptr;
   tlrg_status st{};
   check(tlrg_factorize(context(), h, mode, &cfg, &ws, &fo, &f, &st), st);
-  TlrFactor F = download(f, std::move(A), mode == 0 ? FactorMode::Cholesky : FactorMode::LDLT);
-  tlrg_factor_free(f);
-  return F;
+  // the device factor is released on every exit path (download may throw)
+  std::unique_ptr<tlrg_factor_s, void (*)(tlrg_factor)> guard(f, tlrg_factor_free);
+  return download(f, std::move(A), mode == 0 ? FactorMode::Cholesky : FactorMode::LDLT);
 }
 
 }  // namespace

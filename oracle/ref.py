@@ -61,6 +61,7 @@ def lib():
                                            i64, C.c_int, i64, C.c_int, dp]),
             "ref_matrix_from_parts": (vp, [i64, C.c_int, C.c_double, dp, ip, dp, dp]),
             "ref_matrix_copy": (vp, [vp]),
+            "ref_matrix_flat": (None, [vp, dp, dp, dp]),
             "ref_matrix_free": (None, [vp]),
             "ref_matrix_info": (None, [vp, C.POINTER(i64), ip, ip, dp]),
             "ref_matrix_ranks": (None, [vp, ip]),
@@ -83,6 +84,8 @@ def lib():
             "ref_factor_solve": (C.c_int, [vp, dp, dp]),
             "ref_factor_apply": (C.c_int, [vp, dp, dp]),
             "ref_estimate_2norm_diff": (C.c_double, [vp, vp, C.c_int, u64]),
+            "ref_frob_norm": (C.c_double, [vp]),
+            "ref_estimate_frob_diff": (C.c_double, [vp, vp, C.c_int, u64]),
             "ref_factor_write": (C.c_int, [vp, C.c_char_p]),
             "ref_factor_read": (vp, [C.c_char_p, ip]),
             "ref_sample_left": (C.c_int, [vp, dp, dp, u8p, C.c_int, C.c_int, ip, C.c_int, dp,
@@ -210,16 +213,38 @@ class RefMatrix:
         return (U.reshape(k, self.tile_rows(i)).T.copy(),
                 V.reshape(k, self.tile_rows(j)).T.copy())
 
+    def to_flat(self):
+        """(diag, ranks, U, V) flat arrays in the reference's tile order."""
+        ranks = self.ranks()
+        rows = np.array([self.tile_rows(i) for i in range(self.nb)], dtype=np.int64)
+        nd = int((rows * rows).sum())
+        ii, jj = np.tril_indices(self.nb, -1)
+        order = np.lexsort((jj, ii))  # (i, j) with i ascending, then j
+        ii, jj = ii[order], jj[order]
+        nu = int((rows[ii] * ranks).sum()) if ranks.size else 0
+        nv = int((rows[jj] * ranks).sum()) if ranks.size else 0
+        dg, U, V = np.empty(nd), np.empty(max(nu, 1)), np.empty(max(nv, 1))
+        lib().ref_matrix_flat(self.h, _d(dg), _d(U), _d(V))
+        return dg, ranks, U[:nu], V[:nv]
+
     def to_parts(self):
         """(diag list, ranks, U list, V list) with U/V as (rows, k) arrays."""
-        ranks = self.ranks()
-        diag = [self.diag(k) for k in range(self.nb)]
-        U, V = [], []
+        dg, ranks, Uf, Vf = self.to_flat()
+        diag, off = [], 0
+        for k in range(self.nb):
+            r = self.tile_rows(k)
+            diag.append(dg[off:off + r * r].reshape(r, r).T.copy())
+            off += r * r
+        U, V, ou, ov, t = [], [], 0, 0, 0
         for i in range(1, self.nb):
             for j in range(i):
-                u, v = self.tile(i, j)
-                U.append(u)
-                V.append(v)
+                k = int(ranks[t])
+                ri, rj = self.tile_rows(i), self.tile_rows(j)
+                U.append(Uf[ou:ou + ri * k].reshape(k, ri).T.copy())
+                V.append(Vf[ov:ov + rj * k].reshape(k, rj).T.copy())
+                ou += ri * k
+                ov += rj * k
+                t += 1
         return diag, ranks, U, V
 
     def copy(self):
@@ -270,6 +295,14 @@ def matrix_from_parts(n, b, eps, diag, ranks, U, V) -> RefMatrix:
         Uf = np.zeros(1)
     if Vf.size == 0:
         Vf = np.zeros(1)
+    return RefMatrix(lib().ref_matrix_from_parts(n, b, eps, _d(dg), _i(rk), _d(Uf), _d(Vf)))
+
+
+def matrix_from_flat(n, b, eps, diag, ranks, U, V) -> RefMatrix:
+    """TlrMatrix from the flat layout (diag None: zero diagonal tiles)."""
+    rk = np.ascontiguousarray(ranks, dtype=np.int32)
+    Uf, Vf = f64(U), f64(V)
+    dg = None if diag is None else f64(diag)
     return RefMatrix(lib().ref_matrix_from_parts(n, b, eps, _d(dg), _i(rk), _d(Uf), _d(Vf)))
 
 
@@ -392,6 +425,43 @@ def factor(A: RefMatrix, mode=0, bs=16, eps=1e-6, max_rank=0, window=0, safety=1
 
 def estimate_2norm_diff(A: RefMatrix, F: RefFactor, iters=50, seed=17):
     return lib().ref_estimate_2norm_diff(A.h, F.h, iters, seed)
+
+
+def frob_norm(A: RefMatrix) -> float:
+    """||A||_F, exact tile-wise (same formula as tlrg_frob_norm)."""
+    return lib().ref_frob_norm(A.h)
+
+
+def estimate_frob_diff(A: RefMatrix, F: RefFactor, probes=64, seed=23) -> float:
+    """Hutchinson estimate of ||P A P^T - L L^T||_F (same probes as the device)."""
+    return lib().ref_estimate_frob_diff(A.h, F.h, probes, seed)
+
+
+def accuracy(A: RefMatrix, F: RefFactor, probes=64, seed=23, solve_seed=7):
+    """The accuracy block of bench.py / the parity tests, computed exactly as
+    paper_2108_11932_b200.tlr.accuracy computes it on the device (same probes,
+    same solve vector x = Rng(solve_seed) draws, same rank summary)."""
+    from paper_2108_11932_b200.util import rank_summary
+    fa = frob_norm(A)
+    fd = estimate_frob_diff(A, F, probes, seed)
+    r2 = estimate_2norm_diff(A, F, 50, 17)
+    a2 = A.estimate_2norm(50, 1)
+    x = rng_gaussians(solve_seed, A.n)
+    b = A.matvec(x)
+    xs = F.solve(b)
+    bwd = float(np.linalg.norm(A.matvec(xs) - b) / np.linalg.norm(b))
+    fwd = float(np.linalg.norm(xs - x) / np.linalg.norm(x))
+    m = F._L()
+    try:
+        lr = int(m.memory_report()["low_rank_bytes"])
+        ranks = m.ranks()
+    finally:
+        m.h = None
+    out = {"resid_frob_rel": fd / fa, "resid_frob": fd, "A_frob": fa, "resid_2norm": r2,
+           "resid_2norm_rel": r2 / a2, "backward_err": bwd, "forward_err": fwd,
+           "L_lowrank_bytes": lr}
+    out.update(rank_summary(ranks))
+    return out
 
 
 def _dblocks_flat(A, D):

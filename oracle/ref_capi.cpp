@@ -6,6 +6,8 @@
 // legs may load it, and only as the checker or the CPU baseline.
 //
 // Every entry point forwards to the reference function named beside it.
+#include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -18,6 +20,7 @@
 #include "tlr/geometry.hpp"
 #include "tlr/solve.hpp"
 #include "tlr/tlr_matrix.hpp"
+#include "tlr/util.hpp"
 
 using namespace tlr;
 
@@ -142,7 +145,7 @@ void* ref_matrix_from_parts(long long n, int b, double eps, const double* diag,
   auto* A = new TlrMatrix(n, b);
   A->eps = eps;
   size_t off = 0;
-  for (int i = 0; i < A->nb; ++i) {
+  for (int i = 0; diag && i < A->nb; ++i) {  // diag == null: keep the zero tiles
     int r = A->tile_rows(i);
     A->diag[i] = tile_from(diag + off, r, r);
     off += (size_t)r * r;
@@ -158,6 +161,23 @@ void* ref_matrix_from_parts(long long n, int b, double eps, const double* diag,
       ov += (size_t)A->tile_rows(j) * k;
     }
   return A;
+}
+// the whole matrix in the flat layout of ref_matrix_from_parts (null = skip)
+void ref_matrix_flat(void* h, double* diag, double* U, double* V) {
+  auto* A = static_cast<TlrMatrix*>(h);
+  size_t off = 0, ou = 0, ov = 0;
+  for (int i = 0; i < A->nb; ++i) {
+    if (diag) tile_to(A->diag[i], diag + off);
+    off += A->diag[i].size();
+  }
+  for (int i = 1; i < A->nb; ++i)
+    for (int j = 0; j < i; ++j) {
+      const LowRankTile& t = A->tile(i, j);
+      if (U) tile_to(t.U, U + ou);
+      if (V) tile_to(t.V, V + ov);
+      ou += t.U.size();
+      ov += t.V.size();
+    }
 }
 void* ref_matrix_copy(void* h) { return new TlrMatrix(*static_cast<TlrMatrix*>(h)); }
 void ref_matrix_free(void* h) { delete static_cast<TlrMatrix*>(h); }
@@ -281,6 +301,67 @@ int ref_factor_apply(void* f, const double* x, double* y) {
 double ref_estimate_2norm_diff(void* a, void* f, int iters, unsigned long long seed) {
   return estimate_2norm_diff(*static_cast<TlrMatrix*>(a), *static_cast<TlrFactor*>(f), iters, seed);
 }
+// ---- Frobenius accuracy gate (the reference has none) --
+// Restated here with the reference's public operators so both sides run the
+// identical estimator (device: tlrg_estimate_frob_diff):
+//   ||A||_F^2 exact tile-wise = sum_k ||A_kk||_F^2 + 2 sum_{i>j} tr((U^T U)(V^T V));
+//   ||P A P^T - L L^T||_F^2 ~= (1/p) sum_t ||E g_t||^2, g_t = first n draws of
+//   Rng(tile_seed(seed, 0xF20B, t, 0)), E v as difference_apply (solve.cpp:283-297).
+double ref_frob_norm(void* a) {
+  const TlrMatrix& A = *static_cast<TlrMatrix*>(a);
+  double s = 0.0;
+#pragma omp parallel for reduction(+ : s) schedule(dynamic)
+  for (int k = 0; k < A.nb; ++k) {
+    const DenseTile& d = A.diag[k];
+    for (long long e = 0; e < (long long)d.size(); ++e) s += d.data()[e] * d.data()[e];
+  }
+  const long long nt = (long long)A.lower.size();
+  double l = 0.0;
+#pragma omp parallel for reduction(+ : l) schedule(dynamic)
+  for (long long t = 0; t < nt; ++t) {
+    const LowRankTile& T = A.lower[t];
+    const int r = T.rank();
+    for (int p = 0; p < r; ++p)
+      for (int q = 0; q < r; ++q) {
+        double gu = 0.0, gv = 0.0;
+        for (int i = 0; i < T.U.rows(); ++i) gu += T.U(i, p) * T.U(i, q);
+        for (int i = 0; i < T.V.rows(); ++i) gv += T.V(i, p) * T.V(i, q);
+        l += gu * gv;
+      }
+  }
+  return std::sqrt(s + 2.0 * l);
+}
+double ref_estimate_frob_diff(void* a, void* f, int probes, unsigned long long seed) {
+  const TlrMatrix& A = *static_cast<TlrMatrix*>(a);
+  const TlrFactor& F = *static_cast<TlrFactor*>(f);
+  const std::int64_t n = A.n;
+  auto perm = [&](const std::vector<double>& v, bool inverse) {
+    std::vector<double> out(v.size());
+    for (int k = 0; k < F.L.nb; ++k) {
+      const int src = F.perm[k], rk = F.L.tile_rows(k);
+      if (!inverse)
+        std::memcpy(out.data() + F.L.block_offset(k), v.data() + F.L.block_offset(src), 8 * rk);
+      else
+        std::memcpy(out.data() + F.L.block_offset(src), v.data() + F.L.block_offset(k), 8 * rk);
+    }
+    return out;
+  };
+  double acc = 0.0;
+  for (int t = 0; t < probes; ++t) {
+    Rng rng(tile_seed(seed, 0xF20BULL, (std::uint64_t)t, 0));
+    std::vector<double> g(n);
+    for (double& x : g) x = rng.gaussian();
+    std::vector<double> av = F.perm.empty()
+                                 ? tlr_matvec(A, g)
+                                 : perm(tlr_matvec(A, perm(g, true)), false);
+    std::vector<double> lv = factor_apply(F, g);
+    double e2 = 0.0;
+    for (std::int64_t i = 0; i < n; ++i) e2 += (av[i] - lv[i]) * (av[i] - lv[i]);
+    acc += e2;
+  }
+  return std::sqrt(acc / probes);
+}
+
 int ref_factor_write(void* f, const char* path) {
   try { write_factor(*static_cast<TlrFactor*>(f), path); return 0; }
   catch (const std::exception& e) { return fail(e); }

@@ -93,6 +93,8 @@ SIGNATURES = {
     "tlrg_tlr_matvec": (C.c_int, [vp, dp, dp, C.POINTER(StatusC)]),
     "tlrg_estimate_2norm_diff": (C.c_int, [vp, vp, C.c_int32, C.c_uint64, dp, C.POINTER(StatusC)]),
     "tlrg_estimate_2norm": (C.c_int, [vp, C.c_int32, C.c_uint64, dp, C.POINTER(StatusC)]),
+    "tlrg_frob_norm": (C.c_int, [vp, dp, C.POINTER(StatusC)]),
+    "tlrg_estimate_frob_diff": (C.c_int, [vp, vp, C.c_int32, C.c_uint64, dp, C.POINTER(StatusC)]),
     "tlrg_sample_left": (C.c_int, [vp, dp, dp, u8p, C.c_int32, C.c_int32, ip, C.c_int32, dp,
                                    C.c_int32, C.c_int32, dp, C.POINTER(StatusC)]),
     "tlrg_chol_ara_update": (C.c_int, [vp, dp, dp, u8p, C.c_int32, C.POINTER(AraConfigC),
@@ -100,6 +102,7 @@ SIGNATURES = {
     "tlrg_ara_count": (C.c_int, [vp]),
     "tlrg_ara_tile": (C.c_int, [vp, C.c_int32, ip, dp, dp]),
     "tlrg_ara_free": (None, [vp]),
+    "tlrg_ara_stats": (None, [vp, dp]),
     "tlrg_rng_gaussians": (C.c_int, [vp, C.c_uint64, C.c_int64, dp, C.POINTER(StatusC)]),
     "tlrg_orthog": (C.c_int, [vp, dp, C.c_int32, C.c_int32, dp, C.c_int32, C.c_uint64, dp, dp, dp,
                               dp, C.POINTER(StatusC)]),

@@ -59,10 +59,16 @@ struct Timer {
     cudaEventElapsedTime(&f, a, b);
     return f * 1e-3;
   }
+  // hand the recorded pair to the caller (read later, see column_stats_resolve)
+  std::pair<cudaEvent_t, cudaEvent_t> release() {
+    auto r = std::make_pair(a, b);
+    a = b = nullptr;
+    return r;
+  }
   ~Timer() {
     auto& p = event_pool();
-    p.push_back(a);
-    p.push_back(b);
+    if (a) p.push_back(a);
+    if (b) p.push_back(b);
   }
 };
 __global__ void ara_loop_cond_kernel(cudaGraphConditionalHandle h, int* active, int max_rounds) {
@@ -80,6 +86,23 @@ void ara_loop_cond(cudaGraphConditionalHandle h, int* active, int max_rounds, cu
 }
 }  // namespace
 
+void column_stats_resolve(ColumnStats& cst) {
+  auto fold = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, double& acc) {
+    auto& pool = event_pool();
+    for (auto& e : v) {
+      float f = 0;
+      cudaEventSynchronize(e.second);
+      cudaEventElapsedTime(&f, e.first, e.second);
+      acc += f * 1e-3;
+      pool.push_back(e.first);
+      pool.push_back(e.second);
+    }
+    v.clear();
+  };
+  fold(cst.pending_proj, cst.t_projection);
+  fold(cst.pending_recomp, cst.t_recompress);
+}
+
 bool ara_fused_eligible(int cols, const std::vector<int>& rows, int bs, int window) {
   const char* nf = std::getenv("TLRG_NO_FUSED");
   if (nf && nf[0] == '1') return false;
@@ -92,7 +115,9 @@ bool ara_fused_eligible(int cols, const std::vector<int>& rows, int bs, int wind
     if (r % 2) return false;
     maxrows = std::max(maxrows, r);
   }
-  return ara_fused_supported(maxrows, bs, window);
+  // the shared-memory panel holds both the tile rows (sampling) and the
+  // cols x q exit projection B (recompression): size it for the larger
+  return ara_fused_supported(std::max(maxrows, cols), bs, window);
 }
 
 void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int bs, int maxrows,
@@ -665,7 +690,11 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   // with every tile finished in the fused kernel the projection/recompression
   // phases are empty: leave the panel copy in flight (the column's join waits
   // on this stream) instead of a host round trip just to read the timers
-  if (use_fused && qmax == 0) return;
+  if (use_fused && qmax == 0) {
+    cst.pending_proj.push_back(tp.release());
+    cst.pending_recomp.push_back(tr.release());
+    return;
+  }
   C.wait();
   if (recprof && qmax > 0) {
     int nf = 0;

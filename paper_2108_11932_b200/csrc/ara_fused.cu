@@ -1204,6 +1204,12 @@ bool ara_fused_supported(int maxrows, int bs, int window) {
 void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st) {
   if (T <= 0) return;
   const int bs = args.bs;
+  // the panel stride must cover the exit projection B (cols x q) as well as
+  // the tile rows: a column whose tiles are all shorter than the diagonal
+  // block (n % b != 0, or a multi-GPU share holding only the short last tile)
+  // would otherwise alias B's columns
+  maxrows = std::max(maxrows, args.cols);
+  if (maxrows > MAXROWS) throw CudaError("ara_fused: tile larger than the fused panel");
   long long ysz;
   size_t bytes = fused_smem_bytes(maxrows, bs, args.window, &args.ldy, &ysz);
   args.ysz = ysz;

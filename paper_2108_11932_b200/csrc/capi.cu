@@ -29,6 +29,8 @@ struct tlrg_factor_s {
 struct tlrg_ara_s {
   std::vector<int> i, rank, conv, rounds;
   std::vector<std::vector<double>> Q, B;
+  double t_device = 0, t_fused = 0, flops_fused = 0, flops_ref = 0;
+  long long tile_rounds = 0;
 };
 
 namespace {
@@ -485,14 +487,24 @@ int tlrg_factorize(tlrg_ctx ctx, tlrg_matrix A, int32_t mode, const tlrg_ara_con
                    const tlrg_workspace* ws, const tlrg_factor_options* opts, tlrg_factor* out,
                    tlrg_status* st) {
   return guarded(st, [&] {
+    if (!A || !A->m) config_error("tlrg_factorize: null matrix handle");
+    // take A first (by-value TlrMatrix in the reference: consumed even when the
+    // call throws).  A borrowed view (tlrg_factor_L) still belongs to its
+    // factor: it is deep-copied, like the reference copying F.L into the
+    // by-value argument.
+    std::unique_ptr<Matrix> M;
+    if (A->borrowed) {
+      M = clone(*A->m->ctx, *A->m);
+    } else {
+      M = std::move(A->m);
+      delete A;
+    }
     if (mode != 0 && mode != 1) config_error("tlrg_factorize: mode must be 0 (Chol) or 1 (LDLT)");
     FactorOpts fo;
     if (opts) {
       fo.schur = opts->schur_compensation != 0;
       fo.shift = opts->diag_shift;
     }
-    std::unique_ptr<Matrix> M = std::move(A->m);
-    delete A;  // consumed (by-value TlrMatrix in the reference)
     auto F = factorize(ctx->c, std::move(M), mode, to_cfg(cfg), ws ? ws->parallel_buffers : 64, fo);
     auto* h = new tlrg_factor_s;
     h->f = std::move(F);
@@ -545,14 +557,15 @@ int tlrg_factor_stats(tlrg_factor f, tlrg_stats* o, int32_t* ara_rounds, double*
 }
 int tlrg_factor_dblock(tlrg_factor f, int32_t k, double* d, double* e, uint8_t* s2, int32_t* perm) {
   const Factor& F = *f->f;
-  if (F.mode != 1) return 2;
+  if (F.mode != 1) return 2;  // ConfigError: no D blocks in a Cholesky factor
+  if (k < 0 || k >= F.L->nb) return 2;
   int b = F.L->b, n = F.L->rows(k);
   size_t o = (size_t)k * b;
-  cudaMemcpy(d, F.D.d + o, 8 * n, cudaMemcpyDeviceToHost);
-  if (n > 1) cudaMemcpy(e, F.D.e + o, 8 * (n - 1), cudaMemcpyDeviceToHost);
-  cudaMemcpy(s2, F.D.s2 + o, n, cudaMemcpyDeviceToHost);
-  cudaMemcpy(perm, F.D.perm + o, 4 * n, cudaMemcpyDeviceToHost);
-  return 0;
+  cudaError_t e1 = cudaMemcpy(d, F.D.d + o, 8 * n, cudaMemcpyDeviceToHost);
+  cudaError_t e2 = n > 1 ? cudaMemcpy(e, F.D.e + o, 8 * (n - 1), cudaMemcpyDeviceToHost) : cudaSuccess;
+  cudaError_t e3 = cudaMemcpy(s2, F.D.s2 + o, n, cudaMemcpyDeviceToHost);
+  cudaError_t e4 = cudaMemcpy(perm, F.D.perm + o, 4 * n, cudaMemcpyDeviceToHost);
+  return (e1 || e2 || e3 || e4) ? 1 : 0;
 }
 int tlrg_write_factor(tlrg_factor f, const char* path, tlrg_status* st) {
   int rc = tlrg_write_tlr(&f->Lview, path, st);
@@ -650,10 +663,19 @@ int tlrg_estimate_2norm_diff(tlrg_matrix A, tlrg_factor f, int32_t iters, uint64
     int64_t n = A->m->n;
     double* t = C.buf<double>("pw_t", (size_t)n);
     *out = power_iter(C, n, mix64(seed ^ 0x2fULL), iters, [&](const double* v, double* w) {
-      matvec_device(C, *A->m, v, w);
-      factor_apply_device(C, *f->f, v, t);
-      axpby_device(C, -1.0, t, 1.0, w, n);  // w = A v - L L^T v  (difference_apply)
+      difference_apply_device(C, *A->m, *f->f, v, w, t);
     });
+  });
+}
+int tlrg_frob_norm(tlrg_matrix A, double* out, tlrg_status* st) {
+  return guarded(st, [&] { *out = frob_norm_device(*A->m->ctx, *A->m); });
+}
+int tlrg_estimate_frob_diff(tlrg_matrix A, tlrg_factor f, int32_t probes, uint64_t seed,
+                            double* out, tlrg_status* st) {
+  return guarded(st, [&] {
+    if (probes < 1) config_error("estimate_frob_diff: probes must be >= 1");
+    if (A->m->n != f->f->L->n) config_error("estimate_frob_diff: size mismatch");
+    *out = estimate_frob_diff_device(*f->ctx, *A->m, *f->f, probes, seed);
   });
 }
 int tlrg_estimate_2norm(tlrg_matrix A, int32_t iters, uint64_t seed, double* out, tlrg_status* st) {
@@ -748,12 +770,32 @@ int tlrg_chol_ara_update(tlrg_matrix mh, const double* dd, const double* de, con
     if (!(c.eps > 0)) config_error("chol_ara_update: eps must be positive");
     DUpload du;
     upload_d(du, M, dd, de, ds2);
+    cudaEvent_t ev0, ev1;
+    TLRG_CUDA(cudaEventCreate(&ev0));
+    TLRG_CUDA(cudaEventCreate(&ev1));
+    TLRG_CUDA(cudaEventRecord(ev0, C.st));
     ColumnSetup cs;
     column_setup(C, M, k, du.D, cs);
-    Store store;
+    auto store = std::make_shared<Store>();
+    store->st = C.st_main;
+    store->owner = &C;
     ColumnStats cst;
-    auto res = column_ara(C, M, k, cs, c, store, cst);
+    auto res = column_ara(C, M, k, cs, c, *store, cst);
+    TLRG_CUDA(cudaEventRecord(ev1, C.st));
+    C.sync();
+    column_stats_resolve(cst);
     auto* a = new tlrg_ara_s;
+    {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev0, ev1);
+      a->t_device = ms * 1e-3;
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+      a->t_fused = cst.t_fused;
+      a->flops_fused = cst.flops_fused;
+      a->flops_ref = cst.flops_ref;
+      a->tile_rounds = cst.tile_rounds;
+    }
     int rk = M.rows(k);
     for (auto& r : res) {
       a->i.push_back(r.i);
@@ -782,6 +824,13 @@ int tlrg_ara_tile(tlrg_ara a, int32_t t, int32_t* info, double* Q, double* B) {
   return 0;
 }
 void tlrg_ara_free(tlrg_ara a) { delete a; }
+void tlrg_ara_stats(tlrg_ara a, double* out5) {
+  out5[0] = a->t_device;  // CUDA-event time of the column's ARA (setup .. panel written)
+  out5[1] = (double)a->tile_rounds;
+  out5[2] = a->flops_ref;    // reference-formulation sampling + projection flops
+  out5[3] = a->t_fused;      // fused-kernel event time (0 on the graph path)
+  out5[4] = a->flops_fused;  // algorithmic flops executed in the fused kernel
+}
 
 int tlrg_rng_gaussians(tlrg_ctx ctx, uint64_t seed, int64_t n, double* out, tlrg_status* st) {
   return guarded(st, [&] {

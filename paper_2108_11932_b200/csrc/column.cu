@@ -297,7 +297,6 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
       S.Sref[s] = v;
     }
   };
-  const double m_sref = since();
   const long long Hstride = (long long)b * K;
   double* H = K ? C.buf<double>("H", (size_t)T * Hstride) : nullptr;
   if (cs.d_rank) column_H_dev(C, M, cs, queue, H, Hstride);
@@ -424,8 +423,8 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
   const double m_op = since();
   auto hook = [&] {
     if (prof)
-      std::fprintf(stderr, "colara %d T=%d J=%zu | queue %.3f sref %.3f H %.3f op %.3f launch %.3f ms\n",
-                   k, T, cs.J.size(), m_queue, m_sref, m_h, m_op, since());
+      std::fprintf(stderr, "colara %d T=%d J=%zu | queue %.3f H %.3f op %.3f launch %.3f ms\n",
+                   k, T, cs.J.size(), m_queue, m_h, m_op, since());
     if (on_launch) on_launch();
     fill_sref();
   };

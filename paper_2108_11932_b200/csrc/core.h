@@ -233,7 +233,12 @@ struct ColumnStats {
   double flops_ref = 0;  // reference-formulation sampling+projection flops
   double t_fused = 0, flops_fused = 0;  // fused ARA kernel: event time and in-kernel flops
   long long fused_launches = 0;
+  // event pairs still in flight when column_ara returned (read at the column
+  // join by column_stats_resolve): projection and recompression phases
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_proj, pending_recomp;
 };
+// fold the deferred phase timers into t_projection / t_recompress (after a sync)
+void column_stats_resolve(ColumnStats& cst);
 
 // Column machinery shared by the factorization and the building-block API.
 struct ColumnSetup {
@@ -379,6 +384,14 @@ void matvec_device(Ctx& C, const Matrix& A, const double* x, double* y);
 void factor_apply_device(Ctx& C, const Factor& F, const double* x, double* y);
 void factor_solve_device(Ctx& C, const Factor& F, double* x);  // in place
 double dot_device(Ctx& C, const double* a, const double* b, long long n);
+// w = (P A P^T - L L^T) v in the factor frame (difference_apply, solve.cpp:283-297);
+// t is n doubles of scratch
+void difference_apply_device(Ctx& C, const Matrix& A, const Factor& F, const double* v, double* w,
+                             double* t);
+// ||A||_F exact tile-wise; Hutchinson estimate of ||P A P^T - L L^T||_F
+double frob_norm_device(Ctx& C, const Matrix& A);
+double estimate_frob_diff_device(Ctx& C, const Matrix& A, const Factor& F, int probes,
+                                 uint64_t seed);
 // y <- a*x + b*y on C.st
 void axpby_device(Ctx& C, double a, const double* x, double b, double* y, long long n);
 

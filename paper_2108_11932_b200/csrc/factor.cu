@@ -536,8 +536,6 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     h_ara = hrel();
     S.t_sampling += cst.t_sampling;
     S.t_orthog += cst.t_orthog;
-    S.t_projection += cst.t_projection;
-    S.t_recompress += cst.t_recompress;
     S.flops_ref += cst.flops_ref;
     S.t_fused += cst.t_fused;
     S.flops_fused += cst.flops_fused;
@@ -643,6 +641,9 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     }
     cudaEventRecord(e5.e, C.st);
     C.sync();
+    column_stats_resolve(cst);
+    S.t_projection += cst.t_projection;
+    S.t_recompress += cst.t_recompress;
     S.t_misc += elapsed(e4, e5);
     {
       // device time between columns (host work between e5 of k-1 and e0 of k)

@@ -286,6 +286,104 @@ double dot_device(Ctx& C, const double* a, const double* b, long long n) {
   return h[0];
 }
 
+namespace {
+// ||U V^T||_F^2 = sum_{p,q} (U^T U)_pq (V^T V)_pq, one CTA per low-rank tile,
+// one warp per (p <= q) pair, fixed-order reductions
+struct FrobItem {
+  const double* U;
+  const double* V;
+  int ru, rv, r;
+};
+__global__ void __launch_bounds__(256) lowrank_frob_kernel(const FrobItem* items, double* part) {
+  const FrobItem it = items[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double red[8];
+  double acc = 0.0;
+  const int npairs = it.r * (it.r + 1) / 2;
+  for (int e = warp; e < npairs; e += 8) {
+    int q = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (q * (q + 1) / 2 > e) --q;
+    while ((q + 1) * (q + 2) / 2 <= e) ++q;
+    const int p = e - q * (q + 1) / 2;
+    const double* up = it.U + (long long)p * it.ru;
+    const double* uq = it.U + (long long)q * it.ru;
+    const double* vp = it.V + (long long)p * it.rv;
+    const double* vq = it.V + (long long)q * it.rv;
+    double gu = 0.0, gv = 0.0;
+    for (int i = lane; i < it.ru; i += 32) gu += up[i] * uq[i];
+    for (int i = lane; i < it.rv; i += 32) gv += vp[i] * vq[i];
+    gu = warp_sum(gu);
+    gv = warp_sum(gv);
+    acc += (p == q ? 1.0 : 2.0) * gu * gv;
+  }
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+}  // namespace
+
+double frob_norm_device(Ctx& C, const Matrix& A) {
+  const int nb = A.nb, b = A.b;
+  double* out = C.buf<double>("fn_out", (size_t)nb + 2);
+  for (int k = 0; k < nb; ++k) frob_sq(A.diag + (size_t)k * b * b, (long long)A.rows(k) * A.rows(k),
+                                       out + k, C.st);
+  std::vector<FrobItem> items;
+  for (int i = 1; i < nb; ++i)
+    for (int j = 0; j < i; ++j) {
+      long long t = A.t(i, j);
+      if (A.rank[t]) items.push_back({A.U[t], A.V[t], A.rows(i), A.rows(j), A.rank[t]});
+    }
+  double* part = C.buf<double>("fn_part", items.size() + 1);
+  double* lr = out + nb;
+  if (!items.empty()) {
+    lowrank_frob_kernel<<<(unsigned)items.size(), 256, 0, C.st>>>(C.push(items), part);
+    TLRG_CUDA(cudaGetLastError());
+    sum_kernel<<<1, 32, 0, C.st>>>(part, (int)items.size(), lr);
+  } else {
+    fill_zero(lr, 1, C.st);
+  }
+  C.launches += nb + 2;
+  double* h = C.pinned_dbl((size_t)nb + 1);
+  TLRG_CUDA(cudaMemcpyAsync(h, out, sizeof(double) * (nb + 1), cudaMemcpyDeviceToHost, C.st));
+  C.sync();
+  double s = 0.0;
+  for (int k = 0; k < nb; ++k) s += h[k];
+  return std::sqrt(s + 2.0 * h[nb]);
+}
+
+void difference_apply_device(Ctx& C, const Matrix& A, const Factor& F, const double* v, double* w,
+                             double* t) {
+  matvec_device(C, A, v, w);
+  factor_apply_device(C, F, v, t);
+  axpby_device(C, -1.0, t, 1.0, w, A.n);  // w = A v - L L^T v
+}
+
+// Hutchinson estimate of ||P A P^T - L L^T||_F: probe t
+// is the first n draws of tlr::Rng(tile_seed(seed, 0xF20B, t, 0)), E g as the
+// reference's difference_apply (solve.cpp:283-297); identical estimator to the
+// oracle's ref_estimate_frob_diff, so both sides see the same probes.
+double estimate_frob_diff_device(Ctx& C, const Matrix& A, const Factor& F, int probes,
+                                 uint64_t seed) {
+  const int64_t n = A.n;
+  double* g = C.buf<double>("fr_g", (size_t)n);
+  double* w = C.buf<double>("fr_w", (size_t)n);
+  double* t = C.buf<double>("fr_t", (size_t)n);
+  RngState* rs = C.buf<RngState>("fr_rng", 1);
+  double acc = 0.0;
+  for (int p = 0; p < probes; ++p) {
+    std::vector<uint64_t> s1{tile_seed(seed, 0xF20BULL, (uint64_t)p, 0)};
+    rng_seed(rs, C.push(s1), 1, C.st);
+    rng_draw(rs, nullptr, 1, g, n, n, C.st);
+    difference_apply_device(C, A, F, g, w, t);
+    acc += dot_device(C, w, w, n);
+  }
+  return std::sqrt(acc / probes);
+}
+
 void matvec_device(Ctx& C, const Matrix& A, const double* x, double* y) {
   const int nb = A.nb, b = A.b;
   std::vector<DotItem> d1, d2;

@@ -187,6 +187,10 @@ class TlrMatrix:
     def _consume(self):
         if self.h is None:
             raise ConfigError("TlrMatrix was consumed by a factorization")
+        if self._owner is not None:
+            # borrowed view of a factor's L: the library deep-copies it (the
+            # reference copies F.L into its by-value argument); the view stays valid
+            return self.h
         h, self.h = self.h, None
         return h
 
@@ -207,6 +211,20 @@ class TlrMatrix:
         h = C.c_void_p()
         _call(ctx.lib.tlrg_matrix_upload, ctx.h, n, b, eps, _d(dg), _i(rk) if rk.size else None,
               _d(Uf), _d(Vf), C.byref(h))
+        return TlrMatrix(h, ctx)
+
+    @staticmethod
+    def from_flat(n, b, eps, diag, ranks, U, V, ctx=None) -> "TlrMatrix":
+        """Upload from the reference's flat layout: diag (sum rows(k)^2 or None
+        for zero tiles), ranks[i(i-1)/2+j], U / V payloads concatenated in tile
+        order, column-major (tlrg_matrix_upload)."""
+        ctx = _ctx(ctx)
+        rk = np.ascontiguousarray(ranks, dtype=np.int32)
+        Uf, Vf = _f64(U), _f64(V)
+        h = C.c_void_p()
+        _call(ctx.lib.tlrg_matrix_upload, ctx.h, n, b, eps,
+              None if diag is None else _d(_f64(diag)), _i(rk) if rk.size else None,
+              _d(Uf if Uf.size else np.zeros(1)), _d(Vf if Vf.size else np.zeros(1)), C.byref(h))
         return TlrMatrix(h, ctx)
 
     def tile_rows(self, i):
@@ -299,6 +317,13 @@ def tlr_matvec(A: TlrMatrix, x) -> np.ndarray:
 def estimate_2norm(A: TlrMatrix, iters=50, seed=1) -> float:
     out = C.c_double()
     _call(A.ctx.lib.tlrg_estimate_2norm, A.h, iters, seed, C.byref(out))
+    return out.value
+
+
+def frob_norm(A: TlrMatrix) -> float:
+    """||A||_F, exact tile-wise."""
+    out = C.c_double()
+    _call(A.ctx.lib.tlrg_frob_norm, A.h, C.byref(out))
     return out.value
 
 
@@ -463,6 +488,36 @@ def estimate_2norm_diff(A: TlrMatrix, F: TlrFactor, iters=50, seed=17) -> float:
     return out.value
 
 
+def estimate_frob_diff(A: TlrMatrix, F: "TlrFactor", probes=64, seed=23) -> float:
+    """Hutchinson estimate of ||P A P^T - L L^T||_F (north-star accuracy gate;
+    the oracle's ref_estimate_frob_diff runs the identical estimator)."""
+    out = C.c_double()
+    _call(F.ctx.lib.tlrg_estimate_frob_diff, A.h, F.h, probes, seed, C.byref(out))
+    return out.value
+
+
+def accuracy(A: TlrMatrix, F: "TlrFactor", probes=64, seed=23, solve_seed=7):
+    """The north-star accuracy block, computed the
+    same way as oracle.ref.accuracy: relative Frobenius residual, 2-norm
+    residual, backward / forward solve error, rank distribution of L."""
+    from .util import rank_summary
+    fa = frob_norm(A)
+    fd = estimate_frob_diff(A, F, probes, seed)
+    r2 = estimate_2norm_diff(A, F, 50, 17)
+    a2 = estimate_2norm(A, 50, 1)
+    x = rng_gaussians(solve_seed, A.n, A.ctx)
+    b = tlr_matvec(A, x)
+    xs = factor_solve(F, b)
+    bwd = float(np.linalg.norm(tlr_matvec(A, xs) - b) / np.linalg.norm(b))
+    fwd = float(np.linalg.norm(xs - x) / np.linalg.norm(x))
+    L = F.L
+    out = {"resid_frob_rel": fd / fa, "resid_frob": fd, "A_frob": fa, "resid_2norm": r2,
+           "resid_2norm_rel": r2 / a2, "backward_err": bwd, "forward_err": fwd,
+           "L_lowrank_bytes": int(L.memory_report()["low_rank_bytes"])}
+    out.update(rank_summary(L.ranks()))
+    return out
+
+
 # --------------------------------------------------------- building blocks --
 def _dblocks_flat(A: TlrMatrix, D):
     if D is None:
@@ -515,10 +570,11 @@ class TileApprox:
     rounds_resident: int
 
 
-def chol_ara_update(A: TlrMatrix, D, k, cfg: AraConfig, ws: AraWorkspace = None
-                    ) -> List[TileApprox]:
+def chol_ara_update(A: TlrMatrix, D, k, cfg: AraConfig, ws: AraWorkspace = None,
+                    stats: Optional[dict] = None) -> List[TileApprox]:
     """ara.cpp:302-419: dynamic-batched ARA of every tile below the diagonal of
-    column k.  Returns tiles in ascending i."""
+    column k.  Returns tiles in ascending i.  ``stats`` (a dict) receives the
+    device time and work counters of the call."""
     ws = ws or AraWorkspace()
     dd, de, ds = _dblocks_flat(A, D)
     h = C.c_void_p()
@@ -527,6 +583,11 @@ def chol_ara_update(A: TlrMatrix, D, k, cfg: AraConfig, ws: AraWorkspace = None
           C.byref(w), C.byref(h))
     lib = A.ctx.lib
     out = []
+    if stats is not None:
+        v = np.zeros(5)
+        lib.tlrg_ara_stats(h, _d(v))
+        stats.update(t_device=v[0], tile_rounds=int(v[1]), flops_ref=v[2], t_fused=v[3],
+                     flops_fused=v[4])
     try:
         rk = A.tile_rows(k)
         for t in range(lib.tlrg_ara_count(h)):

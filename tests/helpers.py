@@ -17,8 +17,9 @@ def covariance_ref(ref, n, b, eps, seed=42, kind=G.BALL3D, ell=0.2, nugget=0.0, 
 
 
 def to_gpu(tg, A_ref):
-    diag, ranks, U, V = A_ref.to_parts()
-    return tg.TlrMatrix.from_parts(A_ref.n, A_ref.b, A_ref.eps, diag, ranks, U, V)
+    """The reference-built matrix uploaded unchanged (flat layout)."""
+    diag, ranks, U, V = A_ref.to_flat()
+    return tg.TlrMatrix.from_flat(A_ref.n, A_ref.b, A_ref.eps, diag, ranks, U, V)
 
 
 def dblocks_np(nb, rows, seed):
