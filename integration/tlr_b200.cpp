@@ -3,6 +3,7 @@
 // into oracle/_ref/ for the conformance test; a maintainer adds it to proj/src).
 #include "tlr_b200.hpp"
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -139,7 +140,109 @@ TlrFactor run(TlrMatrix A, const AraConfig& c, const AraWorkspace& w, const Fact
   return download(f, std::move(A), mode == 0 ? FactorMode::Cholesky : FactorMode::LDLT);
 }
 
+// D blocks of the LDL^T columns (dense_kernels.hpp:28-53) in the C ABI's flat
+// nb*b layout; empty when the expression has no D (Chol mode).
+struct FlatD {
+  std::vector<double> d, e;
+  std::vector<uint8_t> s2;
+  FlatD(const TlrMatrix& m, const std::vector<BlockDiagonal>* D, SampleMode mode) {
+    if (mode != SampleMode::LDL || !D) return;
+    const size_t n = (size_t)m.nb * m.b;
+    d.assign(n, 0.0);
+    e.assign(n, 0.0);
+    s2.assign(n, 0);
+    for (int j = 0; j < (int)D->size() && j < m.nb; ++j) {
+      const BlockDiagonal& B = (*D)[j];
+      const size_t o = (size_t)j * m.b;
+      std::copy(B.d.begin(), B.d.end(), d.begin() + o);
+      std::copy(B.e.begin(), B.e.end(), e.begin() + o);
+      std::copy(B.start2x2.begin(), B.start2x2.end(), s2.begin() + o);
+    }
+  }
+  const double* dd() const { return d.empty() ? nullptr : d.data(); }
+  const double* de() const { return e.empty() ? nullptr : e.data(); }
+  const uint8_t* ds2() const { return s2.empty() ? nullptr : s2.data(); }
+};
+
+struct MatrixGuard {
+  tlrg_matrix h;
+  ~MatrixGuard() { tlrg_matrix_free(h); }
+};
+
 }  // namespace
+
+std::vector<TileApprox> chol_ara_update_b200(const TlrMatrix& m,
+                                             const std::vector<BlockDiagonal>* d, int k,
+                                             const AraConfig& c, const AraWorkspace& w,
+                                             SampleMode mode, FactorStats* stats) {
+  if (k + 1 >= m.nb) return {};
+  MatrixGuard A{upload(m)};
+  FlatD D(m, d, mode);
+  tlrg_ara_config cfg{c.block_samples, c.eps, c.max_rank, c.window, c.safety,
+                      c.recompress ? 1 : 0, c.seed};
+  tlrg_workspace ws{w.parallel_buffers, w.dense_buffers, w.subset_capacity};
+  tlrg_ara a = nullptr;
+  tlrg_status st{};
+  check(tlrg_chol_ara_update(A.h, D.dd(), D.de(), D.ds2(), k, &cfg, &ws, &a, &st), st);
+  std::unique_ptr<tlrg_ara_s, void (*)(tlrg_ara)> guard(a, tlrg_ara_free);
+  const int rk = m.tile_rows(k);
+  std::vector<TileApprox> out;
+  for (int i = k + 1; i < m.nb; ++i)  // structurally zero tiles: rank 0, converged, 0 rounds
+    out.push_back({i, DenseTile(m.tile_rows(i), 0), DenseTile(rk, 0), true, 0});
+  for (int t = 0, n = tlrg_ara_count(a); t < n; ++t) {
+    int32_t info[4];
+    tlrg_ara_tile(a, t, info, nullptr, nullptr);
+    TileApprox& T = out[info[0] - k - 1];
+    T.Q = DenseTile(m.tile_rows(info[0]), info[1]);
+    T.B = DenseTile(rk, info[1]);
+    tlrg_ara_tile(a, t, info, T.Q.data(), T.B.data());
+    T.converged = info[2] != 0;
+    T.rounds_resident = info[3];
+  }
+  if (stats) {
+    double s5[5];
+    tlrg_ara_stats(a, s5);
+    stats->t_sampling += s5[0];  // one device region: sampling, projection and orthog fused
+    for (const TileApprox& T : out) stats->tile_rounds_resident += T.rounds_resident;
+  }
+  return out;
+}
+
+std::vector<DenseTile> sample_left_b200(const TlrMatrix& m, const std::vector<BlockDiagonal>* d,
+                                        int k, const std::vector<int>& row_idx,
+                                        const AraWorkspace& ws,
+                                        const std::vector<DenseTile>& omega, SampleMode mode,
+                                        bool transpose) {
+  if (row_idx.empty()) return {};
+  if (ws.parallel_buffers / (int)row_idx.size() < 1)  // ara.cpp:281-284
+    throw ConfigError("sample_left: workspace smaller than one buffer per tile");
+  MatrixGuard A{upload(m)};
+  FlatD D(m, d, mode);
+  const int width = omega.empty() ? 0 : omega[0].cols();
+  std::vector<double> in, out;
+  size_t otot = 0;
+  for (size_t t = 0; t < row_idx.size(); ++t) {
+    in.insert(in.end(), omega[t].data(), omega[t].data() + omega[t].size());
+    otot += (size_t)(transpose ? m.tile_rows(k) : m.tile_rows(row_idx[t])) * width;
+  }
+  in.push_back(0.0);
+  out.assign(otot + 1, 0.0);
+  std::vector<int32_t> rows(row_idx.begin(), row_idx.end());
+  tlrg_status st{};
+  check(tlrg_sample_left(A.h, D.dd(), D.de(), D.ds2(), k, (int32_t)rows.size(), rows.data(),
+                         ws.parallel_buffers, in.data(), width, transpose ? 1 : 0, out.data(), &st),
+        st);
+  std::vector<DenseTile> res;
+  size_t o = 0;
+  for (int i : row_idx) {
+    const int r = transpose ? m.tile_rows(k) : m.tile_rows(i);
+    DenseTile Y(r, width);
+    std::memcpy(Y.data(), out.data() + o, sizeof(double) * r * width);
+    o += (size_t)r * width;
+    res.push_back(std::move(Y));
+  }
+  return res;
+}
 
 TlrFactor tlr_cholesky_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws,
                             const FactorOptions& opts) {

@@ -16,4 +16,16 @@ TlrFactor tlr_cholesky_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspac
                             const FactorOptions& opts = {});
 TlrFactor tlr_ldlt_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws,
                         FactorOptions opts = {});
+
+// Building blocks the reference's own tests call directly (ara.hpp:102-130),
+// evaluated on the device.  Same arguments, results and exceptions.
+std::vector<TileApprox> chol_ara_update_b200(const TlrMatrix& m,
+                                             const std::vector<BlockDiagonal>* d, int k,
+                                             const AraConfig& cfg, const AraWorkspace& ws,
+                                             SampleMode mode, FactorStats* stats = nullptr);
+std::vector<DenseTile> sample_left_b200(const TlrMatrix& m, const std::vector<BlockDiagonal>* d,
+                                        int k, const std::vector<int>& row_idx,
+                                        const AraWorkspace& ws,
+                                        const std::vector<DenseTile>& omega, SampleMode mode,
+                                        bool transpose = false);
 }  // namespace tlr
