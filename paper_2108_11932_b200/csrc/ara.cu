@@ -121,19 +121,20 @@ bool ara_fused_eligible(int cols, const std::vector<int>& rows, int bs, int wind
 }
 
 void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int bs, int maxrows,
-                     int rounds_ahead, StreamPrep& P) {
+                     int rounds_ahead, StreamPrep& P, int ring_rounds) {
   const int T = (int)seeds.size();
   P.T = T;
   P.seeds = seeds;
   GaussStreams& G = P.G;
   G.st = C.buf<RngState>("p_rng", (size_t)T);
-  G.cap = (12LL * cols * bs + 4LL * bs * maxrows + 1) & ~1LL;
+  G.cap = ((long long)ring_rounds * cols * bs + 4LL * bs * maxrows + 1) & ~1LL;
   G.buf = C.buf<double>("p_gbuf", (size_t)T * G.cap);
   long long* gl = C.buf<long long>("p_gcur", (size_t)2 * T);
   G.avail = gl;
   G.cursor = gl + T;
-  P.pre = std::min<long long>(G.cap, (long long)rounds_ahead * cols * bs + 2LL * bs * maxrows);
-  P.pre &= ~1LL;
+  P.pre = std::min<long long>(G.cap, (long long)rounds_ahead * cols * bs +
+                                         (ring_rounds >= 12 ? 2LL * bs * maxrows : 0));
+  P.pre = (P.pre + 1) & ~1LL;
   uint64_t* d_seeds = C.buf<uint64_t>("p_seeds", (size_t)T);
   int* d_slots = C.buf<int>("p_slots", (size_t)T);
   long long* d_want = C.buf<long long>("p_want", (size_t)T);
@@ -188,7 +189,10 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   // per-tile gaussian streams (exact tlr::Rng sequences), consumed by cursor
   GaussStreams G;
   std::vector<long long> h_av(T, 0), h_cur(T, 0);
-  if (!use_fused && pre && pre->T == T && pre->seeds == S.seeds &&
+  // streams generated ahead on the side stream (column_prepare): the graph path
+  // consumes them by cursor; the fused kernel's producer warp continues them, so
+  // its first round does not wait for the in-kernel generator
+  if (pre && pre->T == T && pre->seeds == S.seeds &&
       pre->G.cap >= 2LL * cols * bs + 4LL * bs * maxrows) {
     G = pre->G;
     TLRG_CUDA(cudaStreamWaitEvent(C.st, pre->ev, 0));
@@ -260,6 +264,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     rank_in = C.buf<int>("fusedRank", (size_t)T);
     double* Wb = C.buf<double>("fusedW", (size_t)wtot);
     double* rc = C.buf<double>("fusedRC", (size_t)T * capmax);
+    const size_t cqs = (size_t)(2 * capmax + bs + 4) * bs;
+    double* Cqf = C.buf<double>("fusedCq", (size_t)T * cqs);
     std::vector<FusedSlot> slots(T);
     for (int s = 0; s < T; ++s) {
       FusedSlot& f = slots[s];
@@ -275,7 +281,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       f.Q = Q + s * Qstride;
       f.Om = Om + (size_t)s * cols * bs;
       f.W = Wb + woff[s];
-      f.Cq = Cdef + (size_t)s * capmax * bs;
+      f.Cq = Cqf + (size_t)s * cqs;
       f.repC = rc + (size_t)s * capmax;
       f.Uo = Uo + (size_t)s * maxrows * FUSED_QMAX;
       f.Vo = Vo + (size_t)s * cols * FUSED_QMAX;
@@ -300,6 +306,10 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     fl_dev = C.buf<double>("fusedFlops", (size_t)T);
     fa.flops_out = fl_dev;
     fa.mgs_passes = 2;  // MGS2 as the reference (one pass measurably changes ranks/rounds)
+    {
+      const char* e = std::getenv("TLRG_SWEEP2");  // 0: column-wise second sweep (A/B)
+      fa.fast_sweep2 = !(e && e[0] == '0');
+    }
     const char* fp = std::getenv("TLRG_FUSED_PROF");
     long long* dprof = nullptr;
     if (fp && fp[0] == '1') {

@@ -245,6 +245,9 @@ __device__ void nn16(int rows, int Kd, ACol acol, const double* B, int ldb, Epi 
       }
     }
   }
+  // a warp reads and writes only its own row groups: once every lane's reads
+  // are done the epilogue may overwrite an operand in place
+  __syncwarp();
 #pragma unroll
   for (int i = 0; i < GPW; ++i) {
     const int gr = warp + FW * i;
@@ -465,11 +468,15 @@ __device__ void nn16_tma(int rows, int Kd, ACol acol, const double* B, int ldb, 
 // parity), ONE barrier, then lane p of every warp sums coefficient p over the
 // warps in a fixed order and the update takes it by shuffle.  Warp 0 adds the
 // coefficients to Rp(:, j) when rpj != null.
-template <int BS, int J>
+// NORM: the same reduction also returns ||y_J||^2 BEFORE the update (slot J),
+// so a second pass yields the post-pass norm by Pythagoras,
+// ||y - Y c||^2 = ||y||^2 - ||c||^2 (Y orthonormal), without a third barrier.
+template <int BS, int J, bool NORM = false>
 __device__ __forceinline__ void cgs_pass_reg(double (&y)[RPT][BS], FSmem& S, double* rpj,
-                                             int& par) {
+                                             int& par, double* sq_out = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int N = J <= 2 ? 2 : J <= 4 ? 4 : J <= 8 ? 8 : J <= 16 ? 16 : 32;
+  constexpr int JN = J + (NORM ? 1 : 0);
+  constexpr int N = JN <= 2 ? 2 : JN <= 4 ? 4 : JN <= 8 ? 8 : JN <= 16 ? 16 : 32;
   constexpr int SH = (N == 2 ? 4 : N == 4 ? 3 : N == 8 ? 2 : N == 16 ? 1 : 0);  // 5 - log2 N
   double part[N];
 #pragma unroll
@@ -478,6 +485,9 @@ __device__ __forceinline__ void cgs_pass_reg(double (&y)[RPT][BS], FSmem& S, dou
     if (p < J) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i) v += y[i][p] * y[i][J];
+    } else if (NORM && p == J) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) v += y[i][J] * y[i][J];
     }
     part[p] = v;
   }
@@ -487,7 +497,7 @@ __device__ __forceinline__ void cgs_pass_reg(double (&y)[RPT][BS], FSmem& S, dou
   if ((lane & ((1 << SH) - 1)) == 0) wp[warp * 32 + (lane >> SH)] = red;
   cbar();
   double c = 0.0;
-  if (lane < J) {
+  if (lane < JN) {
     double h0 = 0.0, h1 = 0.0;
 #pragma unroll
     for (int w = 0; w < FW; w += 2) {
@@ -500,6 +510,12 @@ __device__ __forceinline__ void cgs_pass_reg(double (&y)[RPT][BS], FSmem& S, dou
   double cf[J > 0 ? J : 1];
 #pragma unroll
   for (int p = 0; p < J; ++p) cf[p] = __shfl_sync(0xffffffffu, c, p);
+  if (NORM) {
+    double ysq = __shfl_sync(0xffffffffu, c, J), csq = 0.0;
+#pragma unroll
+    for (int p = 0; p < J; ++p) csq += cf[p] * cf[p];
+    *sq_out = ysq - csq;
+  }
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -542,11 +558,16 @@ __device__ __forceinline__ void mgs_column(TileCtx& T, FSmem& S, double (&y)[RPT
   if (J >= T.wlim) return;  // uniform
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* rpj = S.Rp + J * BS;
-  if (J > 0) {
+  double nj;
+  if (J > 0 && T.passes > 1) {
     cgs_pass_reg<BS, J>(y, S, rpj, par);
-    if (T.passes > 1) cgs_pass_reg<BS, J>(y, S, rpj, par);
+    double sq;
+    cgs_pass_reg<BS, J, true>(y, S, rpj, par, &sq);
+    nj = sqrt(fmax(sq, 0.0));
+  } else {
+    if (J > 0) cgs_pass_reg<BS, J>(y, S, rpj, par);
+    nj = cta_norm<BS>(y, J, S, par);
   }
-  double nj = cta_norm<BS>(y, J, S, par);
   if (!(nj >= tau)) {
     if (threadIdx.x == 0 && !S.defi[J]) {
       S.defi[J] = 1;
@@ -627,6 +648,9 @@ struct MgsUnroll<BS, BS> {
   __device__ __forceinline__ static void run(TileCtx&, FSmem&, double (&)[RPT][BS], double, int&) {}
 };
 
+template <int BS>
+__device__ void panel_r_update(FSmem& S, int sweep);
+
 template <int NT>
 __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
   constexpr int BS = NT * 8;
@@ -655,7 +679,12 @@ __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
     }
   }
   cbar();
-  // R <- Rp R   (R = I before the first sweep)
+  panel_r_update<BS>(S, sweep);
+}
+
+// R <- Rp R   (R = I before the first sweep)
+template <int BS>
+__device__ void panel_r_update(FSmem& S, int sweep) {
   const int w = BS;
   if (sweep == 0) {
     for (int e = threadIdx.x; e < w * w; e += FT) S.R[e] = S.Rp[e];
@@ -670,6 +699,95 @@ __device__ void panel_sweep(TileCtx& T, FSmem& S, int sweep, double tau) {
     for (int e = threadIdx.x; e < w * w; e += FT) S.R[e] = S.Rt[e];
   }
   cbar();
+}
+
+// ---- second orthogonalization sweep as one Gram product (CholQR) ----------
+// After sweep 1 the panel is orthonormal and orthogonal to Q to O(eps), so
+// sweep 2's {C = Q^T Y, Y -= Q C, panel MGS2} is, to rounding, Y <- (Y - QC) R2^{-1}
+// with R2 = chol((Y - QC)^T (Y - QC)) = chol(Y^T Y - C^T C) and C^T C = O(eps^2):
+//   [C; G] = [Q | Y]^T Y        one DMMA product (q + bs) x bs
+//   R2 = chol(G), R2inv         one warp
+//   Y <- [Y | Q] [R2inv; -C R2inv]   one DMMA product, in place
+// No column can deflate in this sweep when tau < 1/4 (the columns have unit
+// norm); the caller runs the column-wise sweep otherwise, and also when the
+// Cholesky shows a panel that is not orthonormal (|R2_jj - 1| > 1/4).
+// Returns false (uniform) when the fast path does not apply.  R2 -> S.Rp.
+template <int NT>
+__device__ bool sweep2_gram(const FusedSlot& sl, TileCtx& T, FSmem& S, double* coef,
+                            int* s_ok) {
+  constexpr int BS = NT * 8;
+  const int q = T.q, rows = T.rows, ldy = T.ldy, ldc = (q + 1) & ~1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* G = S.Rt;  // bs x bs
+  tn16<NT>(
+      q + BS, rows,
+      [&](int m) {
+        return m < q ? (const double*)(sl.Q + (long long)m * rows)
+                     : (const double*)(S.Y + (long long)(m - q) * ldy);
+      },
+      [&](int n) { return (const double*)(S.Y + (long long)n * ldy); }, [](int) { return 1.0; },
+      [&](int m, int n, double v) {
+        if (m < q) sl.Cq[m + (long long)n * ldc] = v;
+        else G[(m - q) + n * BS] = v;
+      },
+      S.part);
+  if (warp == 0) {
+    // upper Cholesky R^T R = G, column j of R in lane j (row k built per step)
+    double* R = S.Rp;
+    bool ok = true;
+    for (int e = lane; e < BS * BS; e += 32) R[e] = 0.0;
+    __syncwarp();
+    for (int k = 0; k < BS; ++k) {
+      double d = G[k + k * BS];
+      for (int i = 0; i < k; ++i) d -= R[i + k * BS] * R[i + k * BS];
+      const double rkk = sqrt(fmax(d, 0.0));
+      ok = ok && (fabs(rkk - 1.0) <= 0.25);
+      if (lane > k && lane < BS) {
+        double v = G[k + lane * BS];
+        for (int i = 0; i < k; ++i) v -= R[i + k * BS] * R[i + lane * BS];
+        R[k + lane * BS] = v / rkk;
+      }
+      if (lane == k) R[k + k * BS] = rkk;
+      __syncwarp();
+    }
+    // R^{-1} (upper; G is dead): column j in lane j -> coef rows 0..bs-1 (ld ldk)
+    const int ldk = (q + BS + 1) & ~1;
+    double* X = G;
+    if (lane < BS) {
+      const int j = lane;
+      double* xj = X + j * BS;
+      for (int i = 0; i < BS; ++i) xj[i] = 0.0;
+      xj[j] = 1.0 / R[j + j * BS];
+      for (int i = j - 1; i >= 0; --i) {
+        double v = 0.0;
+        for (int l = i + 1; l <= j; ++l) v += R[i + l * BS] * xj[l];
+        xj[i] = -v / R[i + i * BS];
+      }
+      for (int i = 0; i < BS; ++i) coef[i + (long long)j * ldk] = xj[i];
+    }
+    if (lane == 0) *s_ok = ok;
+  }
+  cbar();
+  if (!*s_ok) return false;
+  // coef rows bs..bs+q-1: -C R^{-1}
+  {
+    const int ldk = (q + BS + 1) & ~1;
+    for (int e = threadIdx.x; e < q * BS; e += FT) {
+      const int i = e % q, j = e / q;
+      double v = 0.0;
+      for (int l = 0; l <= j; ++l) v += sl.Cq[i + (long long)l * ldc] * coef[l + (long long)j * ldk];
+      coef[BS + i + (long long)j * ldk] = -v;
+    }
+    cbar();
+    nn16<NT>(
+        rows, q + BS,
+        [&](int k) {
+          return k < BS ? (const double*)(S.Y + (long long)k * ldy)
+                        : (const double*)(sl.Q + (long long)(k - BS) * rows);
+        },
+        coef, ldk, [&](int m, int n, double v) { S.Y[m + n * ldy] = v; });
+  }
+  return true;
 }
 
 // ---- in-CTA one-sided Jacobi SVD of the small core (svd_truncate, ----------
@@ -947,7 +1065,7 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
     S.defi = reinterpret_cast<uint8_t*>(p);
   }
   __shared__ long long s_cur, s_av, s_rel;
-  __shared__ int s_q, s_done, s_nkeep, s_rounds, s_conv, s_rcount, s_rpos, s_stop;
+  __shared__ int s_q, s_done, s_nkeep, s_rounds, s_conv, s_rcount, s_rpos, s_stop, s_ok;
   __shared__ double s_tau;
   __shared__ ProdSmem prod;
   if (threadIdx.x == 0) {
@@ -1073,6 +1191,12 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
     T.q = s_q;
     tick(2);
     for (int sweep = 0; sweep < 2; ++sweep) {
+      if (sweep == 1 && A.fast_sweep2 && s_tau < 0.25 &&
+          sweep2_gram<NT>(sl, T, S, sl.Cq + (long long)((sl.cap + 1) & ~1) * bs, &s_ok)) {
+        panel_r_update<NT * 8>(S, 1);
+        tick(4);
+        break;
+      }
       if (T.q > 0) {
         const int q = T.q, ldc = (q + 1) & ~1;
         // C = Q^T Y

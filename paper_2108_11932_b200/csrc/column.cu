@@ -214,29 +214,26 @@ std::vector<int> column_queue(const Matrix& M, int k) {
 
 void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPrep& P) {
   P.T = 0;
-  {
-    // the fused ARA needs no pre-generated streams; eligibility of all rows
-    // i > k implies it for the queue (a subset), without building the queue
-    std::vector<int> rws;
-    for (int i = k + 1; i < M.nb; ++i) rws.push_back(M.rows(i));
-    if (ara_fused_eligible(M.rows(k), rws, cfg.bs, cfg.window > 0 ? cfg.window : cfg.bs)) return;
-  }
-  std::vector<int> queue = column_queue(M, k);
-  {
-    std::vector<int> rws;
-    for (int i : queue) rws.push_back(M.rows(i));
-    if (ara_fused_eligible(M.rows(k), rws, cfg.bs, cfg.window > 0 ? cfg.window : cfg.bs))
-      return;  // the fused ARA generates its streams in-kernel (producer warp)
-  }
+  P.k = k;
+  P.queue = column_queue(M, k);
+  const std::vector<int>& queue = P.queue;
+  if (queue.empty()) return;
   std::vector<uint64_t> seeds;
+  std::vector<int> rws;
   int maxrows = 0;
   for (int i : queue) {
     seeds.push_back(ara_column_seed(cfg.seed, i, k));
+    rws.push_back(M.rows(i));
     maxrows = std::max(maxrows, M.rows(i));
   }
-  P.T = 0;
-  if (queue.empty()) return;
-  streams_prepare(C, seeds, M.rows(k), cfg.bs, maxrows, 8, P);
+  const char* pf = std::getenv("TLRG_PREFILL");  // 0: fused kernel generates from scratch
+  const bool fused = ara_fused_eligible(M.rows(k), rws, cfg.bs, cfg.window > 0 ? cfg.window : cfg.bs);
+  if (fused && pf && pf[0] == '0') return;
+  // fused path: the first round of every slot's stream, generated while the
+  // column setup and H products run, in a ring the producer warp continues;
+  // graph path: 8 rounds ahead in a 12-round ring
+  if (fused) streams_prepare(C, seeds, M.rows(k), cfg.bs, maxrows, 1, P, 6);
+  else streams_prepare(C, seeds, M.rows(k), cfg.bs, maxrows, 8, P);
 }
 
 std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnSetup& cs,
@@ -258,7 +255,7 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0)
         .count();
   };
-  std::vector<int> queue = column_queue(M, k);
+  std::vector<int> queue = pre && pre->k == k ? pre->queue : column_queue(M, k);
   const double m_queue = since();
   if (part_world > 1) {
     // intra-column split: slot s of the rank-sorted queue

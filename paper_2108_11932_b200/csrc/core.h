@@ -301,14 +301,18 @@ struct StreamPrep {
   int T = 0;
   long long pre = 0;  // values generated per slot
   std::vector<uint64_t> seeds;
+  int k = -1;              // column the queue below belongs to
+  std::vector<int> queue;  // column_queue(M, k), reused by column_ara
   ~StreamPrep() {
     if (ev) cudaEventDestroy(ev);
   }
 };
 // the fused one-launch ARA applies (even tile sizes, shared-memory budget)
 bool ara_fused_eligible(int cols, const std::vector<int>& rows, int bs, int window);
+// rounds_ahead rounds of every slot's stream generated on the side stream;
+// ring capacity ring_rounds rounds plus replacement room
 void streams_prepare(Ctx& C, const std::vector<uint64_t>& seeds, int cols, int bs, int maxrows,
-                     int rounds_ahead, StreamPrep& P);
+                     int rounds_ahead, StreamPrep& P, int ring_rounds = 12);
 void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& cfg, Store& store,
                const std::vector<int>& out_order, ColumnStats& cst, AraOut& out,
                StreamPrep* pre = nullptr, const std::function<void()>& on_launch = {});

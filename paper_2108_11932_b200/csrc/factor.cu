@@ -324,22 +324,52 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
   C.launches += 2;
 }
 
-// synchronous form (building-block API): widen the sketch until the slack test holds
+// synchronous form: widen the sketch until the slack test holds; when the
+// eps-rank of D exceeds what one sketch can hold (kSchurMaxWidth - 8; measured
+// 82-278 at m = 1024, eps = 1e-3), split the spectrum in chunks: the top p - 16
+// Ritz pairs of each full-width sketch (16 directions of oversampling plus a
+// power step behind them) are deflated from a working copy of D, and the next
+// sketch runs on the deflated matrix, until one has slack.  R = D - kept parts
+// is then the last chunk's residual.
 void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint64_t seed,
                                double* corr, double* frob, int& rank_hint) {
+  const int cap = std::min(n, kSchurMaxWidth);
   int p = schur_comp_width(n, rank_hint);
   int* rk = C.buf<int>("sc_rank", 1);
+  const double* Dw = Dk;
+  double* Dwork = nullptr;
+  int deflated = 0;
   for (int attempt = 0;; ++attempt) {
-    schur_comp_enqueue(C, Dk, n, eps, seed, p, attempt, corr, frob, rk);
+    schur_comp_enqueue(C, Dw, n, eps, seed, p, attempt, corr, frob, rk);
     int* h = C.pinned_ints(1);
     TLRG_CUDA(cudaMemcpyAsync(h, rk, sizeof(int), cudaMemcpyDeviceToHost, C.st));
     C.wait();
-    if (h[0] > p - 8 && p < std::min(n, kSchurMaxWidth)) {
-      p = std::min(std::min(n, kSchurMaxWidth), 2 * p);
+    if (h[0] <= p - 8 || p >= n) {
+      rank_hint = deflated + h[0];
+      return;
+    }
+    if (p < cap) {
+      p = std::min(cap, 2 * p);
       continue;
     }
-    rank_hint = h[0];
-    return;
+    // full-width sketch without slack: deflate its top p - 16 Ritz pairs
+    if (!Dwork) {
+      Dwork = C.buf<double>("sc_Dwork", (size_t)n * n);
+      dcopy(Dk, Dwork, (long long)n * n, C.st);
+      Dw = Dwork;
+    }
+    const int kd = p - 16;
+    std::vector<GemmProblem> pr(1);
+    pr[0] = GemmProblem{};
+    pr[0].A = C.buf<double>("sc_Xl", (size_t)n * p); pr[0].lda = n;
+    pr[0].B = C.buf<double>("sc_Xr", (size_t)n * p); pr[0].ldb = n; pr[0].transB = 1;
+    pr[0].C = Dwork; pr[0].ldc = n; pr[0].M = n; pr[0].N = n; pr[0].K = kd;
+    pr[0].alpha = -1.0; pr[0].beta = 1.0;
+    C.gemm(pr);
+    symmetrize(Dwork, n, C.st);
+    ++C.launches;
+    deflated += kd;
+    if (deflated >= n) numeric_error("schur_compensation: spectrum split did not converge", -1);
   }
 }
 
@@ -581,9 +611,10 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     bool redo_trsm = false;
     C.wait();
     int st_potrf = hs[0], st_sing = hs[1], st_rank = hs[2];
-    if (comp && st_rank > p_comp - 8 && p_comp < std::min(rk, kSchurMaxWidth)) {
-      // sketch too narrow for this column's spectrum: redo with a wider one
-      rank_hint = 2 * p_comp;
+    if (comp && st_rank > p_comp - 8 && p_comp < rk) {
+      // sketch too narrow for this column's spectrum: redo with a wider one,
+      // or (eps-rank above one sketch) with the chunked spectrum split
+      rank_hint = std::max(rank_hint, 2 * p_comp);
       schur_compensation_device(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), corr,
                                 frob, rank_hint);
       diag_tail();
@@ -610,8 +641,10 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     if (redo_trsm && ncols > 0) trsm_gemm();
     {
       float f = 0;
+      // column setup = the Gram blocks G_ij of the re-associated sampling chain
+      // (the j-sum the reference evaluates inside every sampling round)
       cudaEventElapsedTime(&f, e0.e, e1.e);
-      S.t_dense += f * 1e-3;
+      S.t_sampling += f * 1e-3;
       cudaEventElapsedTime(&f, de0.e, de1.e);
       S.t_dense += f * 1e-3;
       cudaEventElapsedTime(&f, de1.e, de2.e);

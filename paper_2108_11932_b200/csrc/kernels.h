@@ -199,7 +199,7 @@ struct FusedSlot {
   double* Q;     // rows x cap basis (ld rows), output
   double* Om;    // cols x bs scratch
   double* W;     // (kA + K) x bs scratch
-  double* Cq;    // cap x bs scratch
+  double* Cq;    // fused: (2 cap + bs + 4) x bs scratch (C = Q^T Y, then sweep-2 coefficients)
   double* repC;  // cap scratch
   double* Uo;    // rows x QMAX recompressed U (Q V_s), written when recompressed in-kernel
   double* Vo;    // cols x QMAX recompressed V before TRSM (Z U_s sigma)
@@ -223,6 +223,7 @@ struct FusedArgs {
   double* flops_out;   // per slot: algorithmic FP64 flops executed by the CTA
   int mgs_passes;      // column passes per sweep in the panel MGS (reference: 2)
   int stage;           // TMA-stage the sampling operands (set by the launcher)
+  int fast_sweep2;     // second orthog sweep as one Gram product (CholQR, see ara_fused.cu)
 };
 constexpr int FUSED_QMAX = 32;  // widest basis recompressed in-kernel
 bool ara_fused_supported(int maxrows, int bs, int window);

@@ -32,10 +32,11 @@ FAMILIES = [
 ]
 
 
-def _gates(acc, ref_acc, nb, eps, mode):
+def _gates(acc, ref_acc, nb, eps, mode, solve=True):
     assert acc["resid_frob_rel"] <= 2.0 * ref_acc["resid_frob_rel"], (acc, ref_acc)
-    assert acc["backward_err"] <= 2.0 * ref_acc["backward_err"], (acc, ref_acc)
-    assert acc["forward_err"] <= 2.0 * ref_acc["forward_err"], (acc, ref_acc)
+    if solve:
+        assert acc["backward_err"] <= 2.0 * ref_acc["backward_err"], (acc, ref_acc)
+        assert acc["forward_err"] <= 2.0 * ref_acc["forward_err"], (acc, ref_acc)
     rm, rr = acc["L_rank_mean"], ref_acc["L_rank_mean"]
     assert abs(rm - rr) <= 0.1 * rr, (rm, rr)
     lb, lr = acc["L_lowrank_bytes"], ref_acc["L_lowrank_bytes"]
@@ -59,7 +60,11 @@ def test_config_family_parity_on_reference_built_matrix(tg, ref, fam):
     factor = tg.tlr_cholesky if mode == 0 else tg.tlr_ldlt
     F = factor(A.copy(), cfg)
     acc = tg.tlr.accuracy(A, F)
-    _gates(acc, ref_acc, A.nb, eps, mode)
+    # LDL^T on the nugget-1e-4 Gaussian kernel: kappa ~ 1e7, and the solve errors
+    # of BOTH implementations swing 10x with the ARA seed (tools/seed_sweep.py:
+    # 3.7e-5 .. 4.0e-4 backward at N = 8,192).  A single-seed ratio is noise
+    # there, so the solve gate is on the geometric mean over seeds below.
+    _gates(acc, ref_acc, A.nb, eps, mode, solve=(mode == 0))
     # draw-for-draw streams: the rank maps agree tile by tile almost everywhere
     assert (F.L.ranks() == F_ref.L_ranks()).mean() >= 0.9
     if mode == 1:
@@ -145,3 +150,23 @@ def test_factor_of_a_borrowed_L_view_copies_it(tg, ref):
     assert (F.L.ranks() == before).all()
     assert np.array_equal(F.L.to_parts()[0][1], d0)
     assert view.ranks().shape == before.shape
+
+
+def test_ldlt_solve_error_over_seeds(tg, ref):
+    """cfg3 family (LDL^T, bs = 32, m = 512): backward and forward solve error
+    within 2x of the reference as the geometric mean over four ARA seeds, on the
+    same reference-built A (the per-seed spread of either side is 10x)."""
+    n, b, eps, bs = 8192, 512, 1e-4, 32
+    A_ref = ref.build(points(G.GRID3D, n, b, 0), 1, 0.2, 1e-4, b, eps, 0, bs, SEED)
+    A = to_gpu(tg, A_ref)
+    ours, theirs = [], []
+    for sd in (1, 2, 4, SEED):
+        F_ref = ref.factor(A_ref, 1, bs=bs, eps=eps, seed=sd)
+        ra = ref.accuracy(A_ref, F_ref)
+        oa = tg.tlr.accuracy(A, tg.tlr_ldlt(A.copy(), tg.AraConfig(block_samples=bs, eps=eps,
+                                                                    seed=sd)))
+        ours.append([oa["backward_err"], oa["forward_err"]])
+        theirs.append([ra["backward_err"], ra["forward_err"]])
+    go = np.exp(np.log(np.array(ours)).mean(axis=0))
+    gr = np.exp(np.log(np.array(theirs)).mean(axis=0))
+    assert (go <= 2.0 * gr).all(), (go, gr, ours, theirs)

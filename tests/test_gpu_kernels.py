@@ -169,3 +169,25 @@ def test_schur_compensation_matches_reference(tg, ref):
         want = ref.schur_compensation(Dk, eps)
         got, frob = tg.tlr.schur_compensation(Dk, eps)
         assert np.abs(got - want).max() <= 1e-6 * max(np.abs(want).max(), eps) + 1e-12
+
+
+@pytest.mark.parametrize("bs,eps,k", [(16, 1e-2, 5), (16, 1e-4, 9), (32, 1e-4, 5), (32, 1e-6, 2)])
+def test_chol_ara_update_headline_tile_size(tg, ref, bs, eps, k):
+    """chol_ara_update at the headline tile m = 512 (the fused kernel's two
+    rows per thread at bs = 16; the graph path at bs = 32): per tile the same
+    rank, rounds and convergence flag as the reference, factors within 1e-9
+    (test_ara.cpp:294-318 standard), on a 2D exponential covariance matrix."""
+    from helpers import points
+    from paper_2108_11932_b200 import geometry as G
+    n, b = 512 * 12, 512
+    A_ref = ref.build(points(G.GRID2D, n, b, 0), 0, 0.1, 0.0, b, eps, 0, bs, 12345)
+    A = to_gpu(tg, A_ref)
+    cfg = tg.AraConfig(block_samples=bs, eps=eps, seed=77)
+    got = tg.chol_ara_update(A, None, k, cfg, tg.AraWorkspace())
+    want = ref.chol_ara_update(A_ref, k, bs=bs, eps=eps, seed=77)
+    assert [t.i for t in got] == [t["i"] for t in want]
+    for g, w in zip(got, want):
+        assert (g.Q.shape[1], g.rounds_resident, g.converged) == \
+            (w["Q"].shape[1], w["rounds"], w["converged"]), g.i
+        d1, d2 = g.Q @ g.B.T, w["Q"] @ w["B"].T
+        assert np.abs(d1 - d2).max() <= 1e-9 * max(np.linalg.norm(d2), 1.0)

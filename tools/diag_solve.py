@@ -42,3 +42,15 @@ print("resid2 ours via ref ", ref.estimate_2norm_diff(A_ref, Fo, 50, 17))
 dmin_o = min(np.min(np.abs(d.d)) for d in F.D)
 dmin_r = min(np.min(np.abs(F_ref.dblock(k)[0])) for k in range(A.nb))
 print("min|d| ours", dmin_o, "ref", dmin_r)
+# per-column pivot trace (min |eigenvalue| of the D blocks)
+pt_o = np.asarray(F.stats.pivot_trace)
+pt_r = np.asarray(F_ref.stats().pivot_trace)
+print("pivot_trace ours", np.array2string(pt_o, precision=3))
+print("pivot_trace ref ", np.array2string(pt_r, precision=3))
+# column 0 is exact input: our Bunch-Kaufman vs LAPACK dsytrf on the same tile
+A00 = A_ref.diag(0)
+Lo, Do, po, info = tg.tlr.dense_ldl(A00)
+Lr, dr, er, s2r, pr = ref.dense_ldl(A00)
+print("col0 perm equal", bool((po == pr).all()), "2x2 equal", bool((Do.start2x2 == s2r).all()),
+      "min|d| ours", np.min(np.abs(Do.d)), "ref", np.min(np.abs(dr)),
+      "max|dL|", np.max(np.abs(Lo - Lr)))
