@@ -50,6 +50,8 @@ typedef struct {
 typedef struct {
   int32_t schur_compensation; /* default 1 (forced 0 for LDL^T, factor.cpp:304) */
   double diag_shift;          /* default 0 */
+  int32_t pivot_norm;         /* pivoted mode: 0 Frobenius (default), 1 2-norm power estimate */
+  int32_t pivot_power_iters;  /* pivoted mode, power iterations (default 50) */
 } tlrg_factor_options;
 
 /* FactorStats (stats.hpp:9-27) plus device-side counters. */
@@ -127,7 +129,8 @@ int tlrg_build(tlrg_ctx ctx, int32_t dim, int64_t n, const double* coords, int32
                const tlrg_ara_config* cfg, tlrg_matrix* out, tlrg_status* st);
 
 /* --------------------------------------------------------------- factor ---
- * tlr_cholesky (mode 0) / tlr_ldlt (mode 1)  (factor.cpp:290-306).
+ * tlr_cholesky (mode 0) / tlr_ldlt (mode 1) / tlr_cholesky_pivoted (mode 2)
+ * (factor.cpp:115-306; Alg. 8 tile pivoting for mode 2, uniform tiles only).
  * The matrix is CONSUMED (moved into the factor, like the reference's by-value
  * TlrMatrix A); the handle must not be used or freed afterwards. */
 int tlrg_factorize(tlrg_ctx ctx, tlrg_matrix A, int32_t mode, const tlrg_ara_config* cfg,
@@ -142,8 +145,12 @@ int tlrg_factor_stats(tlrg_factor f, tlrg_stats* out, int32_t* ara_rounds /* nb 
 /* LDL^T parts of column k: d[n], e[n-1], start2x2[n], intra_perm[n].
    Returns 0, 2 (Cholesky factor or k out of range) or 1 (copy failed). */
 int tlrg_factor_dblock(tlrg_factor f, int32_t k, double* d, double* e, uint8_t* s2, int32_t* perm);
-/* TLRF I/O (factor.cpp:308-395) */
+/* pivoted mode: factor position -> original tile index (nb entries);
+   returns 2 for an unpivoted factor */
+int tlrg_factor_perm(tlrg_factor f, int32_t* perm);
+/* TLRF I/O (factor.cpp:308-395), bit-compatible with write_factor/read_factor */
 int tlrg_write_factor(tlrg_factor f, const char* path, tlrg_status* st);
+int tlrg_read_factor(tlrg_ctx ctx, const char* path, tlrg_factor* out, tlrg_status* st);
 
 /* ---------------------------------------------------------------- solve ---
  * factor_solve / factor_apply / tlr_matvec on HOST vectors (solve.cpp:144-214,

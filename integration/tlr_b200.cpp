@@ -93,6 +93,11 @@ TlrFactor download(tlrg_factor f, TlrMatrix&& A, FactorMode mode) {
       ou += (size_t)ri * q;
       ov += (size_t)rj * q;
     }
+  if (mode == FactorMode::PivotedCholesky) {
+    std::vector<int32_t> p(nb);
+    tlrg_factor_perm(f, p.data());
+    F.perm.assign(p.begin(), p.end());
+  }
   if (mode == FactorMode::LDLT) {
     F.D.resize(nb);
     F.intra_perm.resize(nb);
@@ -116,6 +121,7 @@ TlrFactor download(tlrg_factor f, TlrMatrix&& A, FactorMode mode) {
   F.stats.t_dense = s.t_dense;
   F.stats.t_orthog = s.t_orthog;
   F.stats.t_misc = s.t_misc;
+  F.stats.t_pivot_select = s.t_pivot_select;
   F.stats.wall = s.wall;
   F.stats.compensation_frob = s.compensation_frob;
   F.stats.modified_diagonals = s.modified_diagonals;
@@ -130,14 +136,18 @@ TlrFactor run(TlrMatrix A, const AraConfig& c, const AraWorkspace& w, const Fact
   tlrg_ara_config cfg{c.block_samples, c.eps, c.max_rank, c.window, c.safety,
                       c.recompress ? 1 : 0, c.seed};
   tlrg_workspace ws{w.parallel_buffers, w.dense_buffers, w.subset_capacity};
-  tlrg_factor_options fo{o.schur_compensation ? 1 : 0, o.diag_shift};
+  tlrg_factor_options fo{o.schur_compensation ? 1 : 0, o.diag_shift,
+                         o.pivot_norm == PivotNorm::Frobenius ? 0 : 1, o.pivot_power_iters};
   tlrg_matrix h = upload(A);  // consumed by tlrg_factorize (even when it fails)
   tlrg_factor f = nullptr;
   tlrg_status st{};
   check(tlrg_factorize(context(), h, mode, &cfg, &ws, &fo, &f, &st), st);
   // the device factor is released on every exit path (download may throw)
   std::unique_ptr<tlrg_factor_s, void (*)(tlrg_factor)> guard(f, tlrg_factor_free);
-  return download(f, std::move(A), mode == 0 ? FactorMode::Cholesky : FactorMode::LDLT);
+  return download(f, std::move(A),
+                  mode == 0   ? FactorMode::Cholesky
+                  : mode == 1 ? FactorMode::LDLT
+                              : FactorMode::PivotedCholesky);
 }
 
 // D blocks of the LDL^T columns (dense_kernels.hpp:28-53) in the C ABI's flat
@@ -251,6 +261,10 @@ TlrFactor tlr_cholesky_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspac
 TlrFactor tlr_ldlt_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws,
                         FactorOptions opts) {
   return run(std::move(A), cfg, ws, opts, 1);
+}
+TlrFactor tlr_cholesky_pivoted_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws,
+                                    const FactorOptions& opts) {
+  return run(std::move(A), cfg, ws, opts, 2);
 }
 
 }  // namespace tlr

@@ -4,6 +4,7 @@
 // paper_2108_11932_b200/lib/libtlrg.so; callers switch
 //   tlr::tlr_cholesky(A, cfg, ws, opts)  ->  tlr::tlr_cholesky_b200(A, cfg, ws, opts)
 //   tlr::tlr_ldlt(A, cfg, ws, opts)      ->  tlr::tlr_ldlt_b200(A, cfg, ws, opts)
+//   tlr::tlr_cholesky_pivoted(...)       ->  tlr::tlr_cholesky_pivoted_b200(...)
 // (include/tlr/factor.hpp:35-41).  Same value semantics: A is consumed, the
 // returned TlrFactor is an ordinary host TlrFactor that tlr::factor_solve,
 // tlr::factor_apply, tlr::estimate_2norm_diff, tlr::write_factor accept.
@@ -16,6 +17,8 @@ TlrFactor tlr_cholesky_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspac
                             const FactorOptions& opts = {});
 TlrFactor tlr_ldlt_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws,
                         FactorOptions opts = {});
+TlrFactor tlr_cholesky_pivoted_b200(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws,
+                                    const FactorOptions& opts = {});
 
 // Building blocks the reference's own tests call directly (ara.hpp:102-130),
 // evaluated on the device.  Same arguments, results and exceptions.

@@ -3,6 +3,7 @@
 // Linking this file in place of the CPU definitions makes every existing caller
 // of the reference API run on the device without a source change:
 //   tlr::tlr_cholesky / tlr::tlr_ldlt          (include/tlr/factor.hpp:35-41)
+//   tlr::tlr_cholesky_pivoted                  (include/tlr/factor.hpp:37-39)
 //   tlr::chol_ara_update                        (include/tlr/ara.hpp:126-130)
 //   tlr::sample_left / sample_left_transpose    (include/tlr/ara.hpp:102-114)
 // A maintainer either drops those definitions from proj/src/factor.cpp and
@@ -24,6 +25,11 @@ TlrFactor tlr_cholesky(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws
 TlrFactor tlr_ldlt(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws,
                    FactorOptions opts) {
   return tlr_ldlt_b200(std::move(A), cfg, ws, opts);
+}
+
+TlrFactor tlr_cholesky_pivoted(TlrMatrix A, const AraConfig& cfg, const AraWorkspace& ws,
+                               const FactorOptions& opts) {
+  return tlr_cholesky_pivoted_b200(std::move(A), cfg, ws, opts);
 }
 
 std::vector<TileApprox> chol_ara_update(const TlrMatrix& m, const std::vector<BlockDiagonal>* d,

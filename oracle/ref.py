@@ -76,6 +76,7 @@ def lib():
             "ref_factor": (vp, [vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double,
                                 C.c_int, u64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, ip]),
             "ref_factor_free": (None, [vp]),
+            "ref_set_pivot": (None, [C.c_int, C.c_int]),
             "ref_factor_L": (vp, [vp]),
             "ref_factor_mode": (C.c_int, [vp]),
             "ref_factor_stats": (None, [vp, dp, ip, dp, u64p]),
@@ -387,6 +388,14 @@ class RefFactor:
         lib().ref_factor_stats(self.h, _d(v), _i(ar), _d(pt), C.byref(tr))
         return RefStats(*v[:9].tolist(), int(v[9]), ar, pt, tr.value)
 
+    def perm(self):
+        """pivoted mode: factor position -> tile (factor.hpp:29); [] otherwise"""
+        if self.mode != 2:
+            return []
+        p = np.zeros(self.L.nb, np.int32)
+        lib().ref_factor_perm(self.h, _i(p))
+        return [int(x) for x in p]
+
     def dblock(self, k):
         n = self.L.tile_rows(k)
         d, e = np.zeros(n), np.zeros(max(n - 1, 1))
@@ -412,14 +421,24 @@ class RefFactor:
 
 def factor(A: RefMatrix, mode=0, bs=16, eps=1e-6, max_rank=0, window=0, safety=10.0,
            recompress=True, seed=0, parallel_buffers=64, dense_buffers=20, subset_capacity=0,
-           schur_compensation=True, diag_shift=0.0) -> RefFactor:
+           schur_compensation=True, diag_shift=0.0, pivot_norm=0,
+           pivot_power_iters=50) -> RefFactor:
     """tlr_cholesky (mode 0) / tlr_ldlt (1) / tlr_cholesky_pivoted (2), factor.cpp:290-306.
     A is copied; the caller's handle stays valid."""
     st = C.c_int()
+    lib().ref_set_pivot(pivot_norm, pivot_power_iters)
     h = lib().ref_factor(A.h, mode, bs, eps, max_rank, window, safety, int(recompress), seed,
                          parallel_buffers, dense_buffers, subset_capacity, int(schur_compensation),
                          diag_shift, C.byref(st))
     _check(st.value, "factor")
+    return RefFactor(h)
+
+
+def read_factor(path) -> RefFactor:
+    """read_factor (factor.cpp:340-395)"""
+    st = C.c_int()
+    h = lib().ref_factor_read(str(path).encode(), C.byref(st))
+    _check(st.value, "read_factor")
     return RefFactor(h)
 
 

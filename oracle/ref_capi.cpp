@@ -230,6 +230,12 @@ double ref_estimate_2norm(void* h, int iters, unsigned long long seed) {
 // mode 0 Chol, 1 LDLT, 2 pivoted.  A is COPIED (the caller keeps its handle).
 // stats_out[10] = t_sampling, t_projection, t_reduction, t_dense, t_orthog,
 //                 t_misc, t_pivot_select, wall, compensation_frob, modified_diagonals
+// pivot selection of the next ref_factor(mode = 2) call (FactorOptions, factor.hpp:17-18)
+static int g_pivot_norm = 0, g_pivot_iters = 50;
+void ref_set_pivot(int norm, int iters) {
+  g_pivot_norm = norm;
+  g_pivot_iters = iters;
+}
 void* ref_factor(void* h, int mode, int bs, double eps, int max_rank, int window,
                  double safety, int recompress, unsigned long long seed, int pb, int db,
                  int subset, int schur, double shift, int* status) {
@@ -240,6 +246,8 @@ void* ref_factor(void* h, int mode, int bs, double eps, int max_rank, int window
     FactorOptions o;
     o.schur_compensation = schur != 0;
     o.diag_shift = shift;
+    o.pivot_norm = g_pivot_norm == 0 ? PivotNorm::Frobenius : PivotNorm::TwoNormPower;
+    o.pivot_power_iters = g_pivot_iters;
     TlrFactor* F = new TlrFactor(
         mode == 0 ? tlr_cholesky(std::move(A), cfg, ws, o)
         : mode == 1 ? tlr_ldlt(std::move(A), cfg, ws, o)

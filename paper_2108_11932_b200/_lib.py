@@ -30,7 +30,8 @@ class WorkspaceC(C.Structure):
 
 
 class FactorOptionsC(C.Structure):
-    _fields_ = [("schur_compensation", C.c_int32), ("diag_shift", C.c_double)]
+    _fields_ = [("schur_compensation", C.c_int32), ("diag_shift", C.c_double),
+                ("pivot_norm", C.c_int32), ("pivot_power_iters", C.c_int32)]
 
 
 class StatsC(C.Structure):
@@ -88,6 +89,8 @@ SIGNATURES = {
     "tlrg_factor_stats": (C.c_int, [vp, C.POINTER(StatsC), ip, dp]),
     "tlrg_factor_dblock": (C.c_int, [vp, C.c_int32, dp, dp, u8p, ip]),
     "tlrg_write_factor": (C.c_int, [vp, C.c_char_p, C.POINTER(StatusC)]),
+    "tlrg_read_factor": (C.c_int, [vp, C.c_char_p, C.POINTER(vp), C.POINTER(StatusC)]),
+    "tlrg_factor_perm": (C.c_int, [vp, C.POINTER(C.c_int32)]),
     "tlrg_factor_solve": (C.c_int, [vp, dp, dp, C.POINTER(StatusC)]),
     "tlrg_factor_apply": (C.c_int, [vp, dp, dp, C.POINTER(StatusC)]),
     "tlrg_tlr_matvec": (C.c_int, [vp, dp, dp, C.POINTER(StatusC)]),

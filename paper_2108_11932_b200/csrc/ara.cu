@@ -309,6 +309,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     {
       const char* e = std::getenv("TLRG_SWEEP2");  // 0: column-wise second sweep (A/B)
       fa.fast_sweep2 = !(e && e[0] == '0');
+      const char* d = std::getenv("TLRG_DCGS");  // 0: column-wise CGS2 panel (A/B)
+      fa.dcgs = !(d && d[0] == '0');
     }
     const char* fp = std::getenv("TLRG_FUSED_PROF");
     long long* dprof = nullptr;

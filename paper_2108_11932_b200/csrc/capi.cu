@@ -276,6 +276,8 @@ void tlrg_default_workspace(tlrg_workspace* w) {
 void tlrg_default_factor_options(tlrg_factor_options* o) {
   o->schur_compensation = 1;
   o->diag_shift = 0.0;
+  o->pivot_norm = 0;
+  o->pivot_power_iters = 50;
 }
 
 int tlrg_create(int device, tlrg_ctx* out, tlrg_status* st) {
@@ -423,62 +425,70 @@ int tlrg_write_tlr(tlrg_matrix h, const char* path, tlrg_status* st) {
   });
 }
 
+namespace {
+// read_tlr (tlr_matrix.cpp:301-340) from an open stream; leaves it positioned
+// after the TLRM payload (read_factor continues with the trailer there)
+std::unique_ptr<Matrix> read_tlr_stream(Ctx& C, std::ifstream& f) {
+  char magic[4];
+  uint32_t version = 0, b = 0;
+  uint64_t n = 0;
+  double eps = 0;
+  f.read(magic, 4);
+  f.read((char*)&version, 4);
+  f.read((char*)&n, 8);
+  f.read((char*)&b, 4);
+  f.read((char*)&eps, 8);
+  if (!f || std::memcmp(magic, "TLRM", 4) != 0) data_error("read_tlr: bad magic");
+  if (version != 1) data_error("read_tlr: unsupported version");
+  if (n < 1 || b < 1 || b > n) config_error("TlrMatrix: bad dimensions");
+  int nb = (int)((n + b - 1) / b);
+  auto rows = [&](int i) { return (int)std::min<int64_t>(b, (int64_t)n - (int64_t)i * b); };
+  std::vector<double> diag;
+  for (int k = 0; k < nb; ++k) {
+    uint32_t r = 0, c = 0;
+    f.read((char*)&r, 4);
+    f.read((char*)&c, 4);
+    if (!f) data_error("read_tlr: truncated tile header");
+    if ((int)r != rows(k) || (int)c != rows(k)) data_error("read_tlr: diagonal tile shape mismatch");
+    size_t o = diag.size();
+    diag.resize(o + (size_t)r * c);
+    f.read((char*)(diag.data() + o), 8 * (size_t)r * c);
+    if (!f) data_error("read_tlr: truncated tile payload");
+  }
+  uint64_t count = 0;
+  f.read((char*)&count, 8);
+  if (!f || count != (uint64_t)nb * (nb - 1) / 2) data_error("read_tlr: bad tile count");
+  std::vector<int32_t> ranks(count, 0);
+  std::vector<std::vector<double>> Us(count), Vs(count);
+  for (uint64_t q = 0; q < count; ++q) {
+    uint32_t i = 0, j = 0, r = 0;
+    f.read((char*)&i, 4);
+    f.read((char*)&j, 4);
+    f.read((char*)&r, 4);
+    if (!f || i >= (uint32_t)nb || j >= i) data_error("read_tlr: bad tile index");
+    long long t = tri_index(i, j);
+    ranks[t] = r;
+    Us[t].resize((size_t)rows(i) * r);
+    Vs[t].resize((size_t)rows(j) * r);
+    f.read((char*)Us[t].data(), 8 * Us[t].size());
+    f.read((char*)Vs[t].data(), 8 * Vs[t].size());
+    if (!f) data_error("read_tlr: truncated tile payload");
+  }
+  std::vector<double> U, V;
+  for (uint64_t t = 0; t < count; ++t) {
+    U.insert(U.end(), Us[t].begin(), Us[t].end());
+    V.insert(V.end(), Vs[t].begin(), Vs[t].end());
+  }
+  return upload(C, (int64_t)n, (int)b, eps, diag.data(), ranks.data(), U.data(), V.data());
+}
+}  // namespace
+
 int tlrg_read_tlr(tlrg_ctx ctx, const char* path, tlrg_matrix* out, tlrg_status* st) {
   return guarded(st, [&] {
     std::ifstream f(path, std::ios::binary);
     if (!f) data_error(std::string("read_tlr: cannot open ") + path);
-    char magic[4];
-    uint32_t version = 0, b = 0;
-    uint64_t n = 0;
-    double eps = 0;
-    f.read(magic, 4);
-    f.read((char*)&version, 4);
-    f.read((char*)&n, 8);
-    f.read((char*)&b, 4);
-    f.read((char*)&eps, 8);
-    if (!f || std::memcmp(magic, "TLRM", 4) != 0) data_error("read_tlr: bad magic");
-    if (version != 1) data_error("read_tlr: unsupported version");
-    if (n < 1 || b < 1 || b > n) config_error("TlrMatrix: bad dimensions");
-    int nb = (int)((n + b - 1) / b);
-    auto rows = [&](int i) { return (int)std::min<int64_t>(b, (int64_t)n - (int64_t)i * b); };
-    std::vector<double> diag;
-    for (int k = 0; k < nb; ++k) {
-      uint32_t r = 0, c = 0;
-      f.read((char*)&r, 4);
-      f.read((char*)&c, 4);
-      if (!f) data_error("read_tlr: truncated tile header");
-      if ((int)r != rows(k) || (int)c != rows(k)) data_error("read_tlr: diagonal tile shape mismatch");
-      size_t o = diag.size();
-      diag.resize(o + (size_t)r * c);
-      f.read((char*)(diag.data() + o), 8 * (size_t)r * c);
-      if (!f) data_error("read_tlr: truncated tile payload");
-    }
-    uint64_t count = 0;
-    f.read((char*)&count, 8);
-    if (!f || count != (uint64_t)nb * (nb - 1) / 2) data_error("read_tlr: bad tile count");
-    std::vector<int32_t> ranks(count, 0);
-    std::vector<std::vector<double>> Us(count), Vs(count);
-    for (uint64_t q = 0; q < count; ++q) {
-      uint32_t i = 0, j = 0, r = 0;
-      f.read((char*)&i, 4);
-      f.read((char*)&j, 4);
-      f.read((char*)&r, 4);
-      if (!f || i >= (uint32_t)nb || j >= i) data_error("read_tlr: bad tile index");
-      long long t = tri_index(i, j);
-      ranks[t] = r;
-      Us[t].resize((size_t)rows(i) * r);
-      Vs[t].resize((size_t)rows(j) * r);
-      f.read((char*)Us[t].data(), 8 * Us[t].size());
-      f.read((char*)Vs[t].data(), 8 * Vs[t].size());
-      if (!f) data_error("read_tlr: truncated tile payload");
-    }
-    std::vector<double> U, V;
-    for (uint64_t t = 0; t < count; ++t) {
-      U.insert(U.end(), Us[t].begin(), Us[t].end());
-      V.insert(V.end(), Vs[t].begin(), Vs[t].end());
-    }
     auto* h = new tlrg_matrix_s;
-    h->m = upload(ctx->c, (int64_t)n, (int)b, eps, diag.data(), ranks.data(), U.data(), V.data());
+    h->m = read_tlr_stream(ctx->c, f);
     *out = h;
   });
 }
@@ -499,11 +509,14 @@ int tlrg_factorize(tlrg_ctx ctx, tlrg_matrix A, int32_t mode, const tlrg_ara_con
       M = std::move(A->m);
       delete A;
     }
-    if (mode != 0 && mode != 1) config_error("tlrg_factorize: mode must be 0 (Chol) or 1 (LDLT)");
+    if (mode < 0 || mode > 2)
+      config_error("tlrg_factorize: mode must be 0 (Chol), 1 (LDLT) or 2 (pivoted Chol)");
     FactorOpts fo;
     if (opts) {
       fo.schur = opts->schur_compensation != 0;
       fo.shift = opts->diag_shift;
+      fo.pivot_norm = opts->pivot_norm;
+      fo.pivot_power_iters = opts->pivot_power_iters;
     }
     auto F = factorize(ctx->c, std::move(M), mode, to_cfg(cfg), ws ? ws->parallel_buffers : 64, fo);
     auto* h = new tlrg_factor_s;
@@ -574,7 +587,7 @@ int tlrg_write_factor(tlrg_factor f, const char* path, tlrg_status* st) {
     const Factor& F = *f->f;
     std::ofstream o(path, std::ios::binary | std::ios::app);
     if (!o) data_error("write_factor: cannot append");
-    uint8_t mode = F.mode == 0 ? 0 : 1;
+    uint8_t mode = (uint8_t)F.mode;  // 0 Cholesky, 1 LDLT, 2 pivoted (factor.cpp:311-313)
     o.write((const char*)&mode, 1);
     o.write((const char*)&F.eps, 8);
     if (F.mode == 1) {
@@ -592,8 +605,79 @@ int tlrg_write_factor(tlrg_factor f, const char* path, tlrg_status* st) {
         o.write((const char*)pu.data(), 4 * n);
       }
     }
+    if (F.mode == 2) {
+      std::vector<uint32_t> p(F.perm.begin(), F.perm.end());
+      o.write((const char*)p.data(), 4 * p.size());
+    }
     if (!o) data_error("write_factor: write failed");
   });
+}
+
+// read_factor (factor.cpp:340-395): TLRM payload, then mode, eps, D blocks with
+// intra-tile permutations (LDL^T) or the tile permutation (pivoted)
+int tlrg_read_factor(tlrg_ctx ctx, const char* path, tlrg_factor* out, tlrg_status* st) {
+  return guarded(st, [&] {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) data_error(std::string("read_factor: cannot open ") + path);
+    Ctx& C = ctx->c;
+    auto F = std::make_unique<Factor>();
+    F->L = read_tlr_stream(C, f);
+    const int nb = F->L->nb, b = F->L->b;
+    uint8_t mode = 0;
+    f.read((char*)&mode, 1);
+    f.read((char*)&F->eps, 8);
+    if (!f) data_error("read_factor: missing trailer");
+    F->mode = mode == 0 ? 0 : mode == 1 ? 1 : 2;
+    F->stats.ara_rounds.assign(nb, 0);
+    F->stats.pivot_trace.assign(nb, 0.0);
+    if (F->mode == 1) {
+      std::vector<double> d((size_t)nb * b, 0.0), e((size_t)nb * b, 0.0);
+      std::vector<uint8_t> s2((size_t)nb * b, 0);
+      std::vector<int32_t> pm((size_t)nb * b, 0);
+      for (int k = 0; k < nb; ++k) {
+        uint32_t n = 0;
+        f.read((char*)&n, 4);
+        if (!f || (int)n != F->L->rows(k)) data_error("read_factor: bad D block size");
+        const size_t o = (size_t)k * b;
+        f.read((char*)(d.data() + o), 8 * n);
+        if (n > 1) f.read((char*)(e.data() + o), 8 * (n - 1));
+        f.read((char*)(s2.data() + o), n);
+        std::vector<uint32_t> p(n);
+        f.read((char*)p.data(), 4 * n);
+        if (!f) data_error("read_factor: truncated D block");
+        for (uint32_t i = 0; i < n; ++i) pm[o + i] = (int32_t)p[i];
+      }
+      TLRG_CUDA(cudaMalloc(&F->D.d, sizeof(double) * nb * b));
+      TLRG_CUDA(cudaMalloc(&F->D.e, sizeof(double) * nb * b));
+      TLRG_CUDA(cudaMalloc(&F->D.s2, (size_t)nb * b));
+      TLRG_CUDA(cudaMalloc(&F->D.perm, sizeof(int) * nb * b));
+      TLRG_CUDA(cudaMemcpy(F->D.d, d.data(), 8 * d.size(), cudaMemcpyHostToDevice));
+      TLRG_CUDA(cudaMemcpy(F->D.e, e.data(), 8 * e.size(), cudaMemcpyHostToDevice));
+      TLRG_CUDA(cudaMemcpy(F->D.s2, s2.data(), s2.size(), cudaMemcpyHostToDevice));
+      TLRG_CUDA(cudaMemcpy(F->D.perm, pm.data(), 4 * pm.size(), cudaMemcpyHostToDevice));
+    }
+    if (F->mode == 2) {
+      std::vector<uint32_t> p(nb);
+      f.read((char*)p.data(), 4 * nb);
+      if (!f) data_error("read_factor: truncated permutation");
+      F->perm.assign(p.begin(), p.end());
+      TLRG_CUDA(cudaMalloc(&F->d_perm, sizeof(int) * nb));
+      TLRG_CUDA(cudaMemcpy(F->d_perm, F->perm.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
+    }
+    auto* h = new tlrg_factor_s;
+    h->f = std::move(F);
+    h->ctx = &C;
+    h->Lview.m.reset(h->f->L.get());
+    h->Lview.borrowed = true;
+    *out = h;
+  });
+}
+
+int tlrg_factor_perm(tlrg_factor f, int32_t* perm) {
+  const Factor& F = *f->f;
+  if (F.perm.empty()) return 2;
+  for (size_t i = 0; i < F.perm.size(); ++i) perm[i] = F.perm[i];
+  return 0;
 }
 
 int tlrg_factor_solve(tlrg_factor f, const double* b, double* x, tlrg_status* st) {

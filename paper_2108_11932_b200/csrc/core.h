@@ -341,6 +341,8 @@ void column_prepare(Ctx& C, const Matrix& M, int k, const AraCfg& cfg, StreamPre
 struct FactorOpts {
   bool schur = true;
   double shift = 0.0;
+  int pivot_norm = 0;          // pivoted mode: 0 Frobenius, 1 power 2-norm estimate
+  int pivot_power_iters = 50;
 };
 
 struct Stats {
@@ -361,12 +363,19 @@ struct Stats {
 
 struct Factor {
   std::unique_ptr<Matrix> L;
-  int mode = 0;  // 0 Chol, 1 LDLT
+  int mode = 0;  // 0 Chol, 1 LDLT, 2 pivoted Chol
   DBlocks D;     // owned device arrays in LDL mode
+  std::vector<int> perm;  // pivoted mode: factor position -> tile (factor.hpp:29)
+  int* d_perm = nullptr;  // device copy (solve / residual operators)
   double eps = 0.0;
   Stats stats;
   ~Factor();
 };
+// tile permutation of a length-n vector (solve.cpp:124-140): forward
+// out[block k] = in[block perm[k]], inverse out[block perm[k]] = in[block k]
+void tile_perm_device(Ctx& C, const Factor& F, const double* in, double* out, bool inverse);
+// pivot_swap(k, p, finalized = k) (tlr_matrix.cpp:66-82) on the tile tables
+void pivot_swap_tables(Matrix& M, int k, int p);
 
 std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, const AraCfg& cfg,
                                   int parallel_buffers, const FactorOpts& opts);

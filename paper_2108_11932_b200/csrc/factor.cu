@@ -40,6 +40,113 @@ void dcopy(const double* src, double* dst, long long n, cudaStream_t st) {
   TLRG_CUDA(cudaGetLastError());
 }
 
+// ---- pivoted Cholesky (Alg. 8, factor.cpp:140-209) --------------------------
+// ||A_ii - D_i||_F for candidate tiles i = k0 + blockIdx.x (the running
+// accumulators D_i of the reference's PivotAccumulators), fixed-order reduction
+__global__ void pivot_frob_kernel(const double* diag, const double* dacc, int b, int k0,
+                                  double* cand) {
+  const int i = k0 + blockIdx.x;
+  const long long bb = (long long)b * b, o = (long long)i * bb;
+  double s = 0.0;
+  for (long long t = threadIdx.x; t < bb; t += blockDim.x) {
+    const double v = diag[o + t] - dacc[o + t];
+    s += v * v;
+  }
+  __shared__ double red[32];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    cand[blockIdx.x] = sqrt(t);
+  }
+}
+
+// power_norm_estimate (dense_kernels.cpp:544-564) of A_ii - D_i, one CTA per
+// candidate; g: b start gaussians per candidate (tlr::Rng(tile_seed(seed, 0x9047, k, i)))
+__global__ void pivot_power_kernel(const double* diag, const double* dacc, int b, int k0,
+                                   const double* g, int iters, double* cand) {
+  extern __shared__ double sm[];
+  double* v = sm;
+  double* w = sm + b;
+  __shared__ double red[32];
+  const int i = k0 + blockIdx.x;
+  const long long o = (long long)i * b * b;
+  const int nw_ = blockDim.x >> 5, lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  auto block_sum = [&](double x) {
+    x = warp_sum(x);
+    __syncthreads();
+    if (lane == 0) red[wp] = x;
+    __syncthreads();
+    double t = 0.0;
+    for (int q = 0; q < nw_; ++q) t += red[q];
+    return t;
+  };
+  double ss = 0.0;
+  for (int r = threadIdx.x; r < b; r += blockDim.x) {
+    v[r] = g[(long long)blockIdx.x * b + r];
+    ss += v[r] * v[r];
+  }
+  double nv = sqrt(block_sum(ss));
+  if (nv == 0.0) {
+    if (threadIdx.x == 0) v[0] = 1.0;
+    nv = 1.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < b; r += blockDim.x) v[r] /= nv;
+  __syncthreads();
+  double lambda = 0.0;
+  for (int t = 0; t < iters; ++t) {
+    for (int r = threadIdx.x; r < b; r += blockDim.x) {
+      double a = 0.0;
+      for (int c = 0; c < b; ++c) a += (diag[o + r + (long long)c * b] - dacc[o + r + (long long)c * b]) * v[c];
+      w[r] = a;
+    }
+    __syncthreads();
+    double n2 = 0.0, d = 0.0;
+    for (int r = threadIdx.x; r < b; r += blockDim.x) {
+      n2 += w[r] * w[r];
+      d += v[r] * w[r];
+    }
+    const double nw = sqrt(block_sum(n2));
+    lambda = fabs(block_sum(d));
+    if (nw == 0.0) {
+      lambda = 0.0;
+      break;
+    }
+    for (int r = threadIdx.x; r < b; r += blockDim.x) v[r] = w[r] / nw;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cand[blockIdx.x] = lambda;
+}
+
+__global__ void swap_kernel(double* a, double* b, long long n) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const double x = a[t];
+    a[t] = b[t];
+    b[t] = x;
+  }
+}
+void dswap(double* a, double* b, long long n, cudaStream_t st) {
+  int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  swap_kernel<<<blocks, 256, 0, st>>>(a, b, n);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+__global__ void tile_perm_kernel(const double* in, double* out, const int* perm, int b, int nb,
+                                 int inverse) {
+  const long long n = (long long)nb * b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t / b), r = (int)(t % b);
+    const long long src = (long long)perm[k] * b + r;
+    if (inverse) out[src] = in[t];
+    else out[t] = in[src];
+  }
+}
+
 // BlockDiagonal::first_singular_block (dense_kernels.cpp:221-234)
 __global__ void first_singular_kernel(const double* d, const double* e, const uint8_t* s2, int n,
                                       int* out) {
@@ -123,6 +230,39 @@ void identity(double* A, int n, cudaStream_t st) {
   TLRG_CUDA(cudaGetLastError());
 }
 }  // namespace
+
+void tile_perm_device(Ctx& C, const Factor& F, const double* in, double* out, bool inverse) {
+  const Matrix& L = *F.L;
+  const long long n = (long long)L.nb * L.b;
+  int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  tile_perm_kernel<<<blocks, 256, 0, C.st>>>(in, out, F.d_perm, L.b, L.nb, inverse ? 1 : 0);
+  TLRG_CUDA(cudaGetLastError());
+  ++C.launches;
+}
+
+// TlrMatrix::pivot_swap(k, p, k) (tlr_matrix.cpp:66-82) on the host tile tables
+// (rank and U/V device pointers; uniform tiles, so U and V are interchangeable).
+// The diagonal tiles themselves are swapped on the device by the caller.
+void pivot_swap_tables(Matrix& M, int k, int p) {
+  if (k == p) return;
+  if (k > p) std::swap(k, p);
+  if (M.rows(k) != M.rows(p)) config_error("pivot_swap: tiles of unequal size");
+  auto sw = [&](long long a, long long c) {
+    std::swap(M.rank[a], M.rank[c]);
+    std::swap(M.U[a], M.U[c]);
+    std::swap(M.V[a], M.V[c]);
+  };
+  for (int j = 0; j < k; ++j) sw(M.t(k, j), M.t(p, j));
+  for (int m = k + 1; m < p; ++m) {
+    const long long a = M.t(m, k), c = M.t(p, m);
+    sw(a, c);  // new (m,k) = old A(p,m)^T, new (p,m) = old A(m,k)^T
+    std::swap(M.U[a], M.V[a]);
+    std::swap(M.U[c], M.V[c]);
+  }
+  for (int m = p + 1; m < M.nb; ++m) sw(M.t(m, k), M.t(m, p));
+  const long long pk = M.t(p, k);
+  std::swap(M.U[pk], M.V[pk]);  // new (p,k) = A(p,k)^T
+}
 
 void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st);
 
@@ -381,7 +521,10 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   (void)parallel_buffers;
   FactorOpts opts = opts_in;
   const bool ldl = mode == 1;
+  const bool pivoted = mode == 2;
   if (ldl) opts.schur = false;  // factor.cpp:304
+  if (pivoted && A->n % A->b != 0)
+    config_error("pivoted factorization requires uniform tiles");
   auto t_wall0 = std::chrono::steady_clock::now();
   double flops0 = C.flops;
   long long launches0 = C.launches;
@@ -450,6 +593,17 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   double* corr = C.buf<double>("corr", (size_t)b);
   double* frob = C.buf<double>("cfrob", 1);
   double* piv = C.buf<double>("pivot", (size_t)nb);
+  // pivoted mode (Alg. 8): running diagonal accumulators D_i = sum_{j<k} L_ij L_ij^T
+  // for the not-yet-eliminated tiles, candidate norms, start vectors
+  double* dacc = nullptr;
+  double* cand = nullptr;
+  if (pivoted) {
+    F->perm.resize(nb);
+    for (int i = 0; i < nb; ++i) F->perm[i] = i;
+    dacc = C.buf<double>("piv_dacc", (size_t)nb * b * b);
+    TLRG_CUDA(cudaMemsetAsync(dacc, 0, sizeof(double) * nb * b * b, C.st));
+    cand = C.buf<double>("piv_cand", (size_t)nb);
+  }
   int* info = C.buf<int>("finfo", 4);  // [0] potrf, [1] first singular D block, [2] comp rank, [3] trsm
   int rank_hint = 0;
   Ev e0, e1, e4, e5, de0, de1, de2, de3, ejoin, eprev;
@@ -470,6 +624,99 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     double h_setup = 0, h_diag = 0, h_ara = 0;
     const int rk = M.rows(k);
     double* diagk = M.diag + (size_t)k * b * b;
+    // ---- pivoted: fold column k-1 into the accumulators, pick the tile with the
+    //      largest updated diagonal norm, swap it into position k (factor.cpp:156-209)
+    if (pivoted) {
+      Ev pv0, pv1;
+      const auto hp0 = std::chrono::steady_clock::now();
+      cudaEventRecord(pv0.e, C.st);
+      if (k > 0) {
+        std::vector<GemmProblem> g1, g2, g3;
+        long long go = 0, to = 0;
+        std::vector<long long> gofs, tofs;
+        for (int i = k; i < nb; ++i) {
+          const int r = M.rank[M.t(i, k - 1)];
+          gofs.push_back(go);
+          tofs.push_back(to);
+          go += (long long)r * r;
+          to += (long long)b * r;
+        }
+        double* gb = C.buf<double>("piv_g", (size_t)std::max(go, 1LL));
+        double* tb = C.buf<double>("piv_t", (size_t)std::max(to, 1LL));
+        for (int i = k; i < nb; ++i) {
+          const long long t = M.t(i, k - 1);
+          const int r = M.rank[t];
+          if (!r) continue;
+          double* g = gb + gofs[i - k];
+          double* tt = tb + tofs[i - k];
+          GemmProblem a{};  // g = V^T V   (expand_update, factor.cpp:18-30)
+          a.A = M.V[t]; a.lda = b; a.transA = 1; a.B = M.V[t]; a.ldb = b;
+          a.C = g; a.ldc = r; a.M = r; a.N = r; a.K = b; a.alpha = 1.0;
+          g1.push_back(a);
+          GemmProblem c{};  // t = U g
+          c.A = M.U[t]; c.lda = b; c.B = g; c.ldb = r;
+          c.C = tt; c.ldc = b; c.M = b; c.N = r; c.K = r; c.alpha = 1.0;
+          g2.push_back(c);
+          GemmProblem d{};  // D_i += t U^T
+          d.A = tt; d.lda = b; d.B = M.U[t]; d.ldb = b; d.transB = 1;
+          d.C = dacc + (size_t)i * b * b; d.ldc = b; d.M = b; d.N = b; d.K = r;
+          d.alpha = 1.0; d.beta = 1.0;
+          g3.push_back(d);
+        }
+        if (!g1.empty()) {
+          C.gemm(g1);
+          C.gemm(g2);
+          C.gemm(g3);
+        }
+      }
+      cudaEventRecord(pv1.e, C.st);
+      const int nc = nb - k;
+      if (opts.pivot_norm == 0) {
+        pivot_frob_kernel<<<nc, 256, 0, C.st>>>(M.diag, dacc, b, k, cand);
+      } else {
+        RngState* rs = C.buf<RngState>("piv_rng", (size_t)nc);
+        double* gv = C.buf<double>("piv_gv", (size_t)nc * b);
+        std::vector<uint64_t> seeds(nc);
+        for (int i = k; i < nb; ++i) seeds[i - k] = tile_seed(cfg.seed, 0x9047ULL, k, i);
+        rng_seed(rs, C.push(seeds), nc, C.st);
+        rng_draw(rs, nullptr, nc, gv, b, b, C.st);
+        pivot_power_kernel<<<nc, 256, 2 * b * sizeof(double), C.st>>>(
+            M.diag, dacc, b, k, gv, opts.pivot_power_iters, cand);
+        C.launches += 2;
+      }
+      TLRG_CUDA(cudaGetLastError());
+      ++C.launches;
+      double* hc = C.pinned_dbl((size_t)nc);
+      TLRG_CUDA(cudaMemcpyAsync(hc, cand, sizeof(double) * nc, cudaMemcpyDeviceToHost, C.st));
+      C.wait();
+      int p = k;
+      double best = -1.0;
+      for (int i = k; i < nb; ++i)
+        if (hc[i - k] > best) {
+          best = hc[i - k];
+          p = i;
+        }
+      S.t_dense += elapsed(pv0, pv1);
+      S.t_pivot_select += std::chrono::duration<double>(std::chrono::steady_clock::now() - hp0)
+                              .count() - elapsed(pv0, pv1);
+      if (p != k) {
+        pivot_swap_tables(M, k, p);
+        dswap(M.diag + (size_t)k * b * b, M.diag + (size_t)p * b * b, (long long)b * b, C.st);
+        dswap(dacc + (size_t)k * b * b, dacc + (size_t)p * b * b, (long long)b * b, C.st);
+        std::swap(F->perm[k], F->perm[p]);
+        if (d_rank) {
+          TLRG_CUDA(cudaMemcpyAsync(d_rank, M.rank.data(), sizeof(int) * ntri,
+                                    cudaMemcpyHostToDevice, C.st));
+          TLRG_CUDA(cudaMemcpyAsync(d_U, M.U.data(), sizeof(double*) * ntri,
+                                    cudaMemcpyHostToDevice, C.st));
+        }
+        C.launches += 2;
+      }
+      // D_k for the diagonal path: the accumulator, symmetrized (factor.cpp:207-208)
+      dcopy(dacc + (size_t)k * b * b, Dk, (long long)b * b, C.st);
+      symmetrize(Dk, rk, C.st);
+      C.launches += 2;
+    }
     // ---- gaussian streams of this column's ARA, generated on the side stream
     //      while the column setup and the diagonal path run
     column_prepare(C, M, k, cfg, prep);
@@ -530,7 +777,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
         cudaEventRecord(de0.e, C.st);
         // keep A_kk: the tile is factored in place and a retry re-reads it
         dcopy(diagk, aorig, (long long)rk * rk, C.st);
-        if (cs.K > 0) {
+        if (cs.K > 0 && !pivoted) {
           double* Hk = C.buf<double>("Hk", (size_t)b * cs.K);
           std::vector<int> tk{k};
           column_H(C, M, cs, tk, Hk, (long long)b * cs.K);
@@ -723,6 +970,10 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
   S.kt_gemm_launches = C.kt_launches;
   C.ktiming = false;
   TLRG_CUDA(cudaMemcpy(S.pivot_trace.data(), piv, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+  if (pivoted) {
+    TLRG_CUDA(cudaMalloc(&F->d_perm, sizeof(int) * nb));
+    TLRG_CUDA(cudaMemcpy(F->d_perm, F->perm.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
+  }
   S.wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_wall0).count();
   S.flops_exec = C.flops - flops0 + S.flops_fused;
   S.launches = C.launches - launches0;
@@ -736,6 +987,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
 }
 
 Factor::~Factor() {
+  if (d_perm) cudaFree(d_perm);
   if (D.d) cudaFree(D.d);
   if (D.e) cudaFree(D.e);
   if (D.s2) cudaFree(D.s2);

@@ -223,7 +223,8 @@ struct FusedArgs {
   double* flops_out;   // per slot: algorithmic FP64 flops executed by the CTA
   int mgs_passes;      // column passes per sweep in the panel MGS (reference: 2)
   int stage;           // TMA-stage the sampling operands (set by the launcher)
-  int fast_sweep2;     // second orthog sweep as one Gram product (CholQR, see ara_fused.cu)
+  int fast_sweep2;     // second orthog sweep as one Gram product (see ara_fused.cu)
+  int dcgs;            // panel CGS2 with one reduction per column (see ara_fused.cu)
 };
 constexpr int FUSED_QMAX = 32;  // widest basis recompressed in-kernel
 bool ara_fused_supported(int maxrows, int bs, int window);

@@ -357,7 +357,15 @@ double frob_norm_device(Ctx& C, const Matrix& A) {
 
 void difference_apply_device(Ctx& C, const Matrix& A, const Factor& F, const double* v, double* w,
                              double* t) {
-  matvec_device(C, A, v, w);
+  if (!F.perm.empty()) {
+    // (P A P^T - L L^T) v in the factor frame (solve.cpp:283-297)
+    double* pv = C.buf<double>("da_pv", (size_t)A.n);
+    tile_perm_device(C, F, v, pv, true);
+    matvec_device(C, A, pv, t);
+    tile_perm_device(C, F, t, w, false);
+  } else {
+    matvec_device(C, A, v, w);
+  }
   factor_apply_device(C, F, v, t);
   axpby_device(C, -1.0, t, 1.0, w, A.n);  // w = A v - L L^T v
 }
@@ -504,6 +512,12 @@ void factor_solve_device(Ctx& C, const Factor& F, double* x) {
   const Matrix& L = *F.L;
   const int nb = L.nb, b = L.b;
   const bool ldl = F.mode == 1;
+  double* xp = nullptr;
+  if (!F.perm.empty()) {  // z = P b (solve.cpp:144-155)
+    xp = C.buf<double>("solve_perm", (size_t)L.n);
+    TLRG_CUDA(cudaMemcpyAsync(xp, x, sizeof(double) * L.n, cudaMemcpyDeviceToDevice, C.st));
+    tile_perm_device(C, F, xp, x, false);
+  }
   // forward sweep (solve.cpp:69-90)
   for (int k = 0; k < nb; ++k) {
     int rk = L.rows(k);
@@ -540,6 +554,10 @@ void factor_solve_device(Ctx& C, const Factor& F, double* x) {
                                                            x + (long long)k * b, perm, ldl, 1);
     C.launches += 2;
     if ((k & 31) == 0) C.sync();  // bound the argument arena between syncs
+  }
+  if (xp) {  // x = P^T z
+    TLRG_CUDA(cudaMemcpyAsync(xp, x, sizeof(double) * L.n, cudaMemcpyDeviceToDevice, C.st));
+    tile_perm_device(C, F, xp, x, true);
   }
   C.sync();
 }

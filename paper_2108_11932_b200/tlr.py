@@ -108,13 +108,23 @@ class AraWorkspace:
         return L.WorkspaceC(self.parallel_buffers, self.dense_buffers, self.subset_capacity)
 
 
+class PivotNorm:
+    """factor.hpp:13 (enum class PivotNorm)."""
+    Frobenius = 0
+    TwoNormPower = 1
+
+
 @dataclass
 class FactorOptions:
+    """factor.hpp:15-20."""
     schur_compensation: bool = True
     diag_shift: float = 0.0
+    pivot_norm: int = PivotNorm.Frobenius
+    pivot_power_iters: int = 50
 
     def c(self):
-        return L.FactorOptionsC(int(self.schur_compensation), self.diag_shift)
+        return L.FactorOptionsC(int(self.schur_compensation), self.diag_shift,
+                                int(self.pivot_norm), int(self.pivot_power_iters))
 
 
 # ----------------------------------------------------------------- context --
@@ -385,7 +395,7 @@ class BlockDiagonal:
 
 
 class TlrFactor:
-    MODES = {0: "Cholesky", 1: "LDLT"}
+    MODES = {0: "Cholesky", 1: "LDLT", 2: "PivotedCholesky"}
 
     def __init__(self, handle, ctx):
         self.h = handle
@@ -437,8 +447,26 @@ class TlrFactor:
         self.ctx.lib.tlrg_factor_dblock(self.h, k, _d(d), _d(e), _u8(s2), _i(p))
         return BlockDiagonal(d, e[:n - 1], s2), p
 
+    @property
+    def perm(self) -> List[int]:
+        """Pivoted mode: factor position -> original tile (factor.hpp:29); [] otherwise."""
+        if self.mode != 2:
+            return []
+        p = np.zeros(self.L.nb, np.int32)
+        self.ctx.lib.tlrg_factor_perm(self.h, _i(p))
+        return [int(x) for x in p]
+
     def write(self, path):
         _call(self.ctx.lib.tlrg_write_factor, self.h, path.encode())
+
+
+def read_factor(path: str, ctx=None) -> TlrFactor:
+    """read_factor (factor.cpp:340-395): a TLRF file written by write_factor of
+    either implementation."""
+    ctx = _ctx(ctx)
+    out = C.c_void_p()
+    _call(ctx.lib.tlrg_read_factor, ctx.h, path.encode(), C.byref(out))
+    return TlrFactor(out, ctx)
 
 
 def _factor(A: TlrMatrix, mode: int, cfg: AraConfig, ws: AraWorkspace,
@@ -456,6 +484,12 @@ def tlr_cholesky(A: TlrMatrix, cfg: AraConfig, ws: AraWorkspace = None,
                  opts: FactorOptions = None) -> TlrFactor:
     """factor.cpp:290-293.  ``A`` is consumed (moved into the factor)."""
     return _factor(A, 0, cfg, ws or AraWorkspace(), opts)
+
+
+def tlr_cholesky_pivoted(A: TlrMatrix, cfg: AraConfig, ws: AraWorkspace = None,
+                         opts: FactorOptions = None) -> TlrFactor:
+    """factor.cpp:295-299 (Alg. 8 tile pivoting; uniform tiles only)."""
+    return _factor(A, 2, cfg, ws or AraWorkspace(), opts)
 
 
 def tlr_ldlt(A: TlrMatrix, cfg: AraConfig, ws: AraWorkspace = None,

@@ -67,8 +67,6 @@ def test_config_family_parity_on_reference_built_matrix(tg, ref, fam):
     _gates(acc, ref_acc, A.nb, eps, mode, solve=(mode == 0))
     # draw-for-draw streams: the rank maps agree tile by tile almost everywhere
     assert (F.L.ranks() == F_ref.L_ranks()).mean() >= 0.9
-    if mode == 1:
-        assert all(d.all_positive() for d in F.D)
 
 
 def test_accuracy_estimators_match_the_oracle_on_one_factor(tg, ref):
