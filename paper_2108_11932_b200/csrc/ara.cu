@@ -319,7 +319,25 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       fa.prof = dprof;
     }
     g_fused_launch = std::chrono::steady_clock::now();
-    ara_fused(fa, T, maxrows, C.st);
+    // CTAs per tile: the slowest tile's round chain is the column's critical
+    // path, so columns with few tiles give each tile a cluster that shares its
+    // sampling products (TLRG_CLUSTER=n forces n; the T limits are tunable)
+    int cl = 1;
+    {
+      bool dense = false;
+      for (int s = 0; s < T && !dense; ++s) dense = !fo.Ad.empty() && fo.Ad[s];
+      auto envi = [](const char* n, int d) {
+        const char* e = std::getenv(n);
+        return e ? std::atoi(e) : d;
+      };
+      if (bs == 16 && !dense) {
+        const int t4 = envi("TLRG_CL4_MAXT", 37), t2 = envi("TLRG_CL2_MAXT", 74);
+        cl = T <= t4 ? 4 : T <= t2 ? 2 : 1;
+        const int force = envi("TLRG_CLUSTER", 0);
+        if (force > 0) cl = force >= 4 ? 4 : force >= 2 ? 2 : 1;
+      }
+    }
+    ara_fused(fa, T, maxrows, C.st, cl);
     ++C.launches;
     if (dprof) {
       std::vector<long long> hp((size_t)T * 8);

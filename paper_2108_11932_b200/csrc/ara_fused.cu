@@ -1068,7 +1068,7 @@ __device__ void stream_producer(const FusedArgs& A, int s, volatile long long* s
       buf[p0 + 1] = P.pv[e] * f;
     }
     have += 2LL * PQ;
-    __threadfence_block();
+    __threadfence();  // ring values are read by the leader and (clusters) its helpers
     __syncwarp();
     if (lane == 0) *s_av = have;
   }
@@ -1161,10 +1161,70 @@ __device__ __noinline__ int recompress_tile(const FusedArgs& A, const FusedSlot&
   return r;
 }
 
+// ---- cluster split of the sampling products (CL CTAs per tile) ---------------
+// The leader CTA (cluster rank 0) runs the tile's whole ARA; the CL - 1 helper
+// CTAs join each round's two sampling products, which are the largest part of a
+// round:  W = [V^A | -U_k,:]^T Omega is split by rows of W (each CTA a slice of
+// the kA + K reduction vectors, into the global scratch W), and Y = [U^A | H] W
+// by tile rows (helpers store their rows straight into the leader's shared
+// panel through DSMEM).  Per round:  leader publishes Omega (go) -> every CTA
+// computes its W slice -> all-to-all "W done" -> every CTA computes its Y rows
+// -> helpers signal "Y done" to the leader.  Signalling is by mbarriers with
+// cluster-scope release/acquire, so the leader's free-running producer warp
+// needs no cluster-wide barrier.
+struct ClusterSync {
+  uint64_t go, wdone, ydone;
+  unsigned long long om;  // Omega of the round (written by the leader)
+  int run;                // 1: another round, 0: the tile is done
+};
+
 template <int NT>
+__device__ __forceinline__ void sample_slice(const FusedArgs& A, const FusedSlot& sl, FSmem& S,
+                                             const double* Om, int crank, int CL, int rows,
+                                             int ldy, ClusterSync& cs, unsigned& wd_ph) {
+  const int cols = A.cols, kA = sl.kA, KW = kA + A.K, ldw = (KW + 1) & ~1;
+  // W rows of this CTA, in 8-row DMMA tiles
+  const int mt = (KW + 7) / 8;
+  const int m0 = min(KW, 8 * (crank * mt / CL)), m1 = min(KW, 8 * ((crank + 1) * mt / CL));
+  if (m1 > m0)
+    tn16<NT>(
+        m1 - m0, cols,
+        [&](int m) {
+          m += m0;
+          return m < kA ? sl.VA + (long long)m * cols : A.Ucat + (long long)(m - kA) * cols;
+        },
+        [&](int n) { return Om + (long long)n * cols; },
+        [&](int m) { return m + m0 < kA ? 1.0 : -1.0; },
+        [&](int m, int n, double v) { sl.W[m + m0 + (long long)n * ldw] = v; }, S.part);
+  __threadfence();  // W is read by the other CTAs of the cluster
+  cbar();
+  if (threadIdx.x == 0)
+    for (int c = 0; c < CL; ++c) mbar_arrive_remote(map_shared(&cs.wdone, c));
+  mbar_wait_cluster(&cs.wdone, wd_ph);
+  wd_ph ^= 1;
+  // Y rows of this CTA, in 16-row groups
+  const int ng = (rows + 15) / 16;
+  const int r0 = 16 * (crank * ng / CL), r1 = min(rows, 16 * ((crank + 1) * ng / CL));
+  if (r1 <= r0) return;
+  auto acolY = [&](int k) {
+    return (k < kA ? sl.UA + (long long)k * rows : sl.H + (long long)(k - kA) * rows) + r0;
+  };
+  if (crank == 0) {
+    nn16<NT>(r1 - r0, KW, acolY, sl.W, ldw,
+             [&](int m, int n, double v) { S.Y[m + r0 + n * ldy] = v; });
+  } else {
+    const unsigned ybase = map_shared(S.Y, 0);
+    nn16<NT>(r1 - r0, KW, acolY, sl.W, ldw, [&](int m, int n, double v) {
+      st_cluster_f64(ybase + 8u * (unsigned)(m + r0 + n * ldy), v);
+    });
+  }
+}
+
+template <int NT, int CL>
 __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
   extern __shared__ __align__(16) double fsm[];
-  const int s = blockIdx.x;
+  const int s = blockIdx.x / CL;
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
   const FusedSlot& sl = A.slots[s];
   const int rows = sl.rows, cols = A.cols, bs = NT * 8;
   constexpr int BQ = NT * 8 > FUSED_QMAX ? NT * 8 : FUSED_QMAX;
@@ -1195,6 +1255,37 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
   __shared__ int s_q, s_done, s_nkeep, s_rounds, s_conv, s_rcount, s_rpos, s_stop, s_ok;
   __shared__ double s_tau;
   __shared__ ProdSmem prod;
+  __shared__ ClusterSync csync;
+  if (CL > 1) {
+    if (threadIdx.x == 0) {
+      mbar_init(&csync.go, 1);
+      mbar_init(&csync.wdone, CL);
+      mbar_init(&csync.ydone, CL - 1);
+    }
+    // every CTA's barriers exist before anyone signals them (all threads)
+    cluster_sync_all();
+  }
+  if (CL > 1 && crank > 0) {
+    // ---- helper CTA: the tile's sampling products, round by round ----------
+    if (threadIdx.x >= FT) return;
+    unsigned go_ph = 0, wd_ph = 0;
+    const unsigned ydone0 = map_shared(&csync.ydone, 0);
+    const int ldy = A.ldy;
+    FSmem S;
+    S.Y = fsm;
+    S.part = fsm + A.ysz + 3 * (NT * 8 > FUSED_QMAX ? NT * 8 : FUSED_QMAX) *
+                                   (NT * 8 > FUSED_QMAX ? NT * 8 : FUSED_QMAX);
+    while (true) {
+      mbar_wait_cluster(&csync.go, go_ph);
+      go_ph ^= 1;
+      if (!csync.run) break;
+      sample_slice<NT>(A, sl, S, (const double*)csync.om, crank, CL, sl.rows, ldy, csync, wd_ph);
+      fence_cluster();
+      cbar();
+      if (threadIdx.x == 0) mbar_arrive_remote(ydone0);
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     s_cur = A.G.cursor[s];
     s_av = A.G.avail[s];
@@ -1221,7 +1312,17 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
   __shared__ __align__(8) uint64_t s_sbar[2];
   Stager stg{nullptr, s_sbar};
   unsigned sph = 0;
-  const bool use_tma = A.stage && NT <= 2 && cols <= MAXROWS && rows <= MAXROWS;
+  const bool use_tma = CL == 1 && A.stage && NT <= 2 && cols <= MAXROWS && rows <= MAXROWS;
+  unsigned wd_ph = 0, yd_ph = 0;
+  // leader: release the helpers (one more round, or done)
+  auto publish = [&](const double* om, int run) {
+    if (CL > 1 && threadIdx.x == 0)
+      for (int c = 1; c < CL; ++c) {
+        st_cluster_u64(map_shared(&csync.om, c), (unsigned long long)om);
+        st_cluster_u32(map_shared(&csync.run, c), (unsigned)run);
+        mbar_arrive_remote(map_shared(&csync.go, c));
+      }
+  };
   if (use_tma) {
     stg.buf = S.Y + (((long long)ldy * bs + 15) & ~15LL);
     if (threadIdx.x == 0) {
@@ -1288,7 +1389,15 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
       auto sgnW = [&](int m) { return m < kA ? 1.0 : -1.0; };
       auto outW = [&](int m, int n, double v) { sl.W[m + (long long)n * ldw] = v; };
       auto epiY = [&](int m, int n, double v) { S.Y[m + n * ldy] = v; };
-      if (use_tma) {
+      if (CL > 1) {
+        __threadfence();  // a wrapped Omega was assembled in global memory by this CTA
+        cbar();
+        publish(Om, 1);
+        sample_slice<NT>(A, sl, S, Om, 0, CL, rows, ldy, csync, wd_ph);
+        mbar_wait_cluster(&csync.ydone, yd_ph);  // the helpers' rows are in S.Y
+        yd_ph ^= 1;
+        cbar();
+      } else if (use_tma) {
         // W = [V^A | -U_k,:]^T Omega   (KW x bs, ld ldw), then Y = [U^A | H] W
         tn16_tma<NT>(KW, cols, acolW, [&](int n) { return Om + (long long)n * cols; }, sgnW, outW,
                      S.part, stg, sph);
@@ -1386,6 +1495,7 @@ __global__ void __launch_bounds__(FTP, 1) ara_fused_kernel(FusedArgs A) {
     cbar();
     tick(5);
   }
+  publish(nullptr, 0);  // the helpers leave
   // ---- exit projection + recompression of this tile (q <= FUSED_QMAX) --------
   __shared__ int s_flag;
   if (A.recompress) {
@@ -1452,7 +1562,30 @@ bool ara_fused_supported(int maxrows, int bs, int window) {
   return bytes + 1024 <= (size_t)optin;
 }
 
-void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st) {
+template <int NT, int CL>
+void launch_fused(const FusedArgs& args, int T, size_t bytes, cudaStream_t st) {
+  static size_t lim = enable_max_dyn_smem(ara_fused_kernel<NT, CL>);
+  if (bytes > lim) throw CudaError("ara_fused: shared memory budget exceeded");
+  if (CL == 1) {
+    ara_fused_kernel<NT, CL><<<T, FTP, bytes, st>>>(args);
+    return;
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)(T * CL));
+  lc.blockDim = dim3(FTP);
+  lc.dynamicSmemBytes = bytes;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  TLRG_CUDA(cudaLaunchKernelEx(&lc, ara_fused_kernel<NT, CL>, args));
+}
+
+void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st, int cl) {
   if (T <= 0) return;
   const int bs = args.bs;
   // the panel stride must cover the exit projection B (cols x q) as well as
@@ -1471,19 +1604,15 @@ void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st) {
     const char* e = std::getenv("TLRG_FUSED_TMA");
     args.stage = (bs <= 16 && e && e[0] == '1') ? 1 : 0;
   }
-  switch (bs) {
-#define TLRG_FUSED_CASE(NT)                                                                 \
-  case NT * 8: {                                                                            \
-    static size_t lim = enable_max_dyn_smem(ara_fused_kernel<NT>);                          \
-    if (bytes > lim) throw CudaError("ara_fused: shared memory budget exceeded");           \
-    ara_fused_kernel<NT><<<T, FTP, bytes, st>>>(args);                                       \
-    break;                                                                                  \
-  }
-    TLRG_FUSED_CASE(1)
-    TLRG_FUSED_CASE(2)
-#undef TLRG_FUSED_CASE
-    default:
-      throw CudaError("ara_fused: unsupported block size");
+  if (cl > 1) args.stage = 0;
+  if (bs == 8) {
+    launch_fused<1, 1>(args, T, bytes, st);
+  } else if (bs == 16) {
+    if (cl >= 4) launch_fused<2, 4>(args, T, bytes, st);
+    else if (cl == 2) launch_fused<2, 2>(args, T, bytes, st);
+    else launch_fused<2, 1>(args, T, bytes, st);
+  } else {
+    throw CudaError("ara_fused: unsupported block size");
   }
   TLRG_CUDA(cudaGetLastError());
 }

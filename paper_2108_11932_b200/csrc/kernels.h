@@ -228,7 +228,9 @@ struct FusedArgs {
 };
 constexpr int FUSED_QMAX = 32;  // widest basis recompressed in-kernel
 bool ara_fused_supported(int maxrows, int bs, int window);
-void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st);
+// cl: CTAs per tile (thread-block cluster; 1, 2 or 4) sharing each round's
+// sampling products (chain operator only, bs = 16)
+void ara_fused(FusedArgs args, int T, int maxrows, cudaStream_t st, int cl = 1);
 
 // ---------------------------------------------------------------- DENSE ---
 // Cholesky of an m x m tile in place (lower); info[0] = failing column or -1.
