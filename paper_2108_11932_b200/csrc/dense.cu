@@ -251,43 +251,62 @@ __global__ void __launch_bounds__(1024) cholqr_kernel(const double* G, int p, in
     }
     __syncthreads();
   }
-  // output R (upper, row-major in smem -> column-major p x p); a dropped pivot
-  // leaves a zero row/column, which cholqr_apply turns into a zero basis column
-  for (int e = tid; e < p * p; e += blockDim.x) {
-    const int i = e % p, j = e / p;
-    Rinv[e] = (i <= j) ? R[i * ld + j] : 0.0;
+  // R^{-1} (upper), column j by thread j (back substitution against R in smem);
+  // a dropped pivot leaves a zero row/column, i.e. a zero basis column
+  if (tid < p) {
+    const int j = tid;
+    double* x = Rinv + (long long)j * p;
+    for (int i = j + 1; i < p; ++i) x[i] = 0.0;
+    const double rjj = R[j * ld + j];
+    x[j] = rjj != 0.0 ? 1.0 / rjj : 0.0;
+    for (int i = j - 1; i >= 0; --i) {
+      const double rii = R[i * ld + i];
+      double s0 = 0.0, s1 = 0.0;
+      int l = i + 1;
+      for (; l + 1 <= j; l += 2) {
+        s0 += R[i * ld + l] * x[l];
+        s1 += R[i * ld + l + 1] * x[l + 1];
+      }
+      if (l <= j) s0 += R[i * ld + l] * x[l];
+      x[i] = rii != 0.0 ? -(s0 + s1) / rii : 0.0;
+    }
   }
 }
 
-// Y <- Y R^{-1}: row r of Y solves q R = y (forward substitution over the p
-// columns), one thread per row, R staged in shared memory
-__global__ void __launch_bounds__(128) cholqr_apply_kernel(double* Y, int n, int p,
-                                                           const double* R) {
-  extern __shared__ double rs[];
-  for (int e = threadIdx.x; e < p * p; e += blockDim.x) rs[e] = R[e];
-  __syncthreads();
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  double q[160];
-  for (int j = 0; j < p; ++j) {
-    const double rjj = rs[j + j * p];
-    double s0 = Y[r + (long long)j * n], s1 = 0.0;
-    int i = 0;
-    for (; i + 1 < j; i += 2) {
-      s0 -= q[i] * rs[i + j * p];
-      s1 -= q[i + 1] * rs[i + 1 + j * p];
-    }
-    if (i < j) s0 -= q[i] * rs[i + j * p];
-    q[j] = rjj != 0.0 ? (s0 + s1) / rjj : 0.0;
+// Y <- Y R^{-1} (upper R^{-1} from cholqr_kernel): a CTA owns 16 rows, stages
+// them in shared memory and writes the products back in place; every output
+// y_rj = sum_{i <= j} y_ri Rinv_ij is one thread's short dot product
+constexpr int CQ_ROWS = 16;
+__global__ void __launch_bounds__(256) cholqr_apply_kernel(double* Y, int n, int p,
+                                                           const double* Rinv) {
+  extern __shared__ double ys[];  // CQ_ROWS x p
+  const int r0 = blockIdx.x * CQ_ROWS, nr = min(CQ_ROWS, n - r0);
+  for (int e = threadIdx.x; e < CQ_ROWS * p; e += blockDim.x) {
+    const int r = e % CQ_ROWS, j = e / CQ_ROWS;
+    ys[e] = r < nr ? Y[r0 + r + (long long)j * n] : 0.0;
   }
-  for (int j = 0; j < p; ++j) Y[r + (long long)j * n] = q[j];
+  __syncthreads();
+  for (int e = threadIdx.x; e < CQ_ROWS * p; e += blockDim.x) {
+    const int r = e % CQ_ROWS, j = e / CQ_ROWS;
+    const double* x = Rinv + (long long)j * p;
+    double s0 = 0.0, s1 = 0.0;
+    int i = 0;
+    for (; i + 1 <= j; i += 2) {
+      s0 += ys[r + i * CQ_ROWS] * __ldg(x + i);
+      s1 += ys[r + (i + 1) * CQ_ROWS] * __ldg(x + i + 1);
+    }
+    if (i <= j) s0 += ys[r + i * CQ_ROWS] * __ldg(x + i);
+    if (r < nr) Y[r0 + r + (long long)j * n] = s0 + s1;
+  }
 }
-void cholqr_apply(double* Y, int n, int p, const double* R, cudaStream_t st) {
+void cholqr_apply(double* Y, int n, int p, const double* Rinv, cudaStream_t st) {
   static size_t lim = enable_max_dyn_smem(cholqr_apply_kernel);
   (void)lim;
-  cholqr_apply_kernel<<<(n + 127) / 128, 128, (size_t)p * p * 8, st>>>(Y, n, p, R);
+  cholqr_apply_kernel<<<(n + CQ_ROWS - 1) / CQ_ROWS, 256, (size_t)CQ_ROWS * p * 8, st>>>(Y, n, p,
+                                                                                      Rinv);
   TLRG_CUDA(cudaGetLastError());
 }
+
 
 void cholqr_factor(const double* G, int p, int n, int shift, double* Rinv, cudaStream_t st) {
   static size_t lim = enable_max_dyn_smem(cholqr_kernel);

@@ -245,8 +245,8 @@ void trsm_panel(const double* L, int n, double* B, long long nrhs, const int* pe
                 cudaStream_t st, double* work = nullptr /* n x nrhs, LDL mode */);
 // (shifted) Cholesky-QR step: R^T R = G (+ shift), Rinv = R^{-1}, p <= 160
 void cholqr_factor(const double* G, int p, int n, int shift, double* Rinv, cudaStream_t st);
-// Y (n x p, ld n) <- Y R^{-1} row by row (R upper p x p from cholqr_factor's
-// R output); columns with a dropped pivot are zeroed.  In place.
+// Y (n x p, ld n) <- Y R^{-1} (R^{-1} upper p x p from cholqr_factor's
+// Rinv output); columns with a dropped pivot are zeroed.  In place.
 void cholqr_apply(double* Y, int n, int p, const double* R, cudaStream_t st);
 // X_bb = L_bb^{-1} for diagonal blocks (offset, length <= 32) of an n x n lower L
 void trtri_base(const double* L, int n, double* X, const int* d_offs, const int* d_lens,
