@@ -1,5 +1,6 @@
 // Grouped FP64 DMMA GEMM launcher and the argument-table arena.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -52,7 +53,8 @@ void DescArena::release_retired() {
 }
 
 template <int BM, int BN>
-static GemmPlan plan_grouped(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
+static GemmPlan plan_grouped(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st,
+                             int big = 0) {
   std::vector<GemmProblem> live;
   live.reserve(probs.size());
   long long tiles = 0;
@@ -65,6 +67,7 @@ static GemmPlan plan_grouped(std::vector<GemmProblem>& probs, DescArena& desc, c
   }
   GemmPlan plan;
   plan.bn = BN;
+  plan.big = big;
   if (tiles == 0) return plan;
   if (tiles > 0x7fffffffLL) throw std::runtime_error("grouped_gemm: too many tiles");
   std::vector<int> owner((size_t)tiles);
@@ -79,16 +82,56 @@ static GemmPlan plan_grouped(std::vector<GemmProblem>& probs, DescArena& desc, c
   return plan;
 }
 
+// the large-tile kernels pay off once every problem of the list is big: a
+// ragged list of thin problems keeps the 64-row tiles (better load balance)
+static int big_config(const std::vector<GemmProblem>& probs) {
+  const char* e = std::getenv("TLRG_GEMM_BIG");  // 0: never use the large tiles (A/B)
+  if (e && e[0] == '0') return 0;
+  long long work = 0, t64 = 0, t32 = 0;
+  int minM = 1 << 30, minN = 1 << 30, maxN = 0;
+  for (auto& p : probs) {
+    if (p.M <= 0 || p.N <= 0) continue;
+    minM = std::min(minM, p.M);
+    minN = std::min(minN, p.N);
+    maxN = std::max(maxN, p.N);
+    work += (long long)p.M * p.N * std::max(p.K, 1);
+    t64 += (long long)((p.M + 127) / 128) * ((p.N + 63) / 64);
+    t32 += (long long)((p.M + 127) / 128) * ((p.N + 31) / 32);
+  }
+  // large tiles only with about a wave of them (148 SMs): fewer CTAs than that
+  // leave SMs idle and the 64 x 32 kernel wins
+  if (work < (1LL << 24) || minM < 128) return 0;
+  if (minN >= 64 && t64 >= 120) return 1;
+  if (maxN <= 32 && minN >= 24 && t32 >= 120) return 2;
+  return 0;
+}
+
 GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
   int maxN = 0;
   for (auto& p : probs)
     if (p.M > 0) maxN = std::max(maxN, p.N);
+  const int big = big_config(probs);
+  if (big == 1) return plan_grouped<128, 64>(probs, desc, st, 1);
+  if (big == 2) return plan_grouped<128, 32>(probs, desc, st, 2);
   return maxN <= 16 ? plan_grouped<64, 16>(probs, desc, st) : plan_grouped<64, 32>(probs, desc, st);
+}
+
+template <int BM, int BN, int WGM, int WGN, int ST>
+static void launch_big(const GemmPlan& p, cudaStream_t st) {
+  constexpr size_t bytes = (size_t)ST * 16 * ((BM + 4) + (BN + 4)) * sizeof(double);
+  static size_t lim = enable_max_dyn_smem(grouped_gemm_big_kernel<BM, BN, WGM, WGN, ST>);
+  (void)lim;
+  grouped_gemm_big_kernel<BM, BN, WGM, WGN, ST>
+      <<<(unsigned)p.tiles, 32 * WGM * WGN, bytes, st>>>(p.d, p.owner);
 }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t st) {
   if (p.tiles == 0) return;
-  if (p.bn == 16)
+  if (p.big == 1)
+    launch_big<128, 64, 4, 2, 3>(p, st);
+  else if (p.big == 2)
+    launch_big<128, 32, 4, 1, 3>(p, st);
+  else if (p.bn == 16)
     grouped_gemm_kernel<64, 16><<<(unsigned)p.tiles, 128, 0, st>>>(p.d, p.owner);
   else
     grouped_gemm_kernel<64, 32><<<(unsigned)p.tiles, 128, 0, st>>>(p.d, p.owner);

@@ -191,4 +191,154 @@ __global__ void __launch_bounds__(128) grouped_gemm_kernel(const GemmProblem* __
       }
 }
 
+// ---- large-tile variant: BM x BN x 16, WGM x WGN warps of 32 x (BN/WGN),
+// STAGES-deep cp.async pipeline, 16-byte copies where the operand is contiguous
+// along the shared tile's fast axis (A not transposed: m; B transposed: n) and
+// 16-byte aligned, 8-byte copies otherwise.  Used for problem lists with large
+// tiles (the diagonal SYRK D_k = H_k U_k^T, the compensation sketch products at
+// m = 1024, the bs = 32 sampling products), where the 64 x 32 kernel's
+// per-element copies and 2:1 load:DMMA ratio cap it well below the pipe.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int BM, int BN, int WGM, int WGN, int STAGES>
+__global__ void __launch_bounds__(32 * WGM * WGN) grouped_gemm_big_kernel(
+    const GemmProblem* __restrict__ probs, const int* __restrict__ owner) {
+  constexpr int NT = 32 * WGM * WGN, BK = 16, SA = BM + 4, SB = BN + 4;
+  constexpr int WM = BM / WGM, WN = BN / WGN, FM = WM / 8, FN = WN / 8;
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                        // STAGES x BK x SA
+  double* Bs = gsm + STAGES * BK * SA;     // STAGES x BK x SB
+  __shared__ __align__(16) GemmProblem sP;
+  __shared__ int s_go;
+  {
+    const int pidx = owner[blockIdx.x];
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(probs + pidx);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sP);
+    constexpr int W = sizeof(GemmProblem) / 8;
+    if (threadIdx.x < W) dst[threadIdx.x] = src[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int go = 1;
+      if (sP.skip && *sP.skip) go = 0;
+      if (go && sP.Mp) sP.M = min(sP.M, *sP.Mp);
+      if (go && sP.Kp) sP.K = min(sP.K, *sP.Kp);
+      const int local = blockIdx.x - sP.tile_start;
+      if (go && (local / sP.tiles_n) * BM >= sP.M) go = 0;
+      s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) return;
+  }
+  const GemmProblem P = sP;
+  const int local = blockIdx.x - P.tile_start;
+  const int m0 = (local / P.tiles_n) * BM, n0 = (local % P.tiles_n) * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp / WGN) * WM, wn = (warp % WGN) * WN;
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nk = (P.K + BK - 1) / BK;
+  auto load = [&](int stage, int k0) {
+    double* as = As + stage * BK * SA;
+    double* bs = Bs + stage * BK * SB;
+    if (!P.transA) {
+      // pairs (gm, gm + 1) of one k are contiguous in both
+      for (int e = tid; e < BM * BK / 2; e += NT) {
+        const int mm = 2 * (e % (BM / 2)), kk = e / (BM / 2);
+        const int gm = m0 + mm, gk = k0 + kk;
+        const double* src = P.A + gm + (long long)gk * P.lda;
+        const bool v0 = gm < P.M && gk < P.K, v1 = gm + 1 < P.M && gk < P.K;
+        if (v0 && v1 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+          cp_async16(&as[kk * SA + mm], src, 16);
+        } else {
+          cp_async8(&as[kk * SA + mm], v0 ? src : P.A, v0);
+          cp_async8(&as[kk * SA + mm + 1], v1 ? src + 1 : P.A, v1);
+        }
+      }
+    } else {
+      for (int e = tid; e < BM * BK; e += NT) {
+        const int kk = e % BK, mm = e / BK;
+        const int gm = m0 + mm, gk = k0 + kk;
+        const bool v = gm < P.M && gk < P.K;
+        cp_async8(&as[kk * SA + mm], v ? P.A + gk + (long long)gm * P.lda : P.A, v);
+      }
+    }
+    if (P.transB) {
+      for (int e = tid; e < BN * BK / 2; e += NT) {
+        const int nn = 2 * (e % (BN / 2)), kk = e / (BN / 2);
+        const int gk = k0 + kk, gn = n0 + nn;
+        const double* src = P.B + gn + (long long)gk * P.ldb;
+        const bool v0 = gk < P.K && gn < P.N, v1 = gk < P.K && gn + 1 < P.N;
+        if (v0 && v1 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+          cp_async16(&bs[kk * SB + nn], src, 16);
+        } else {
+          cp_async8(&bs[kk * SB + nn], v0 ? src : P.B, v0);
+          cp_async8(&bs[kk * SB + nn + 1], v1 ? src + 1 : P.B, v1);
+        }
+      }
+    } else {
+      for (int e = tid; e < BN * BK; e += NT) {
+        const int kk = e % BK, nn = e / BK;
+        const int gk = k0 + kk, gn = n0 + nn;
+        const bool v = gk < P.K && gn < P.N;
+        cp_async8(&bs[kk * SB + nn], v ? P.B + gk + (long long)gn * P.ldb : P.B, v);
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load(s, s * BK);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait_n<STAGES - 2>();
+    __syncthreads();
+    {
+      const int kn = kt + STAGES - 1;
+      if (kn < nk) load(kn % STAGES, kn * BK);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * BK * SA;
+    const double* bs = Bs + (kt % STAGES) * BK * SB;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double af[FM], bf[FN];
+#pragma unroll
+      for (int i = 0; i < FM; ++i) af[i] = as[(ks + t4) * SA + wm + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[j] = bs[(ks + t4) * SB + wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait_n<0>();
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gm = m0 + wm + i * 8 + g;
+        const int gn = n0 + wn + j * 8 + 2 * t4 + h;
+        if (gm < P.M && gn < P.N) {
+          double* c = P.C + gm + (long long)gn * P.ldc;
+          double v = P.alpha * acc[i][j][h];
+          if (P.beta != 0.0) v += P.beta * *c;
+          *c = v;
+        }
+      }
+}
+
 }  // namespace tlrg

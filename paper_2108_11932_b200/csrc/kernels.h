@@ -21,6 +21,7 @@ struct GemmPlan {
   const GemmProblem* d = nullptr;
   const int* owner = nullptr;  // per-CTA problem index
   int n = 0, tiles = 0, bn = 32;
+  int big = 0;  // 0: 64 x bn tiles; 1: 128 x 64 (8 warps); 2: 128 x 32 (4 warps)
 };
 GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st);
 void gemm_launch(const GemmPlan& p, cudaStream_t st);

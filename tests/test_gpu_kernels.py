@@ -10,7 +10,11 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("M,N,K,ta,tb", [(64, 32, 16, 0, 0), (100, 17, 33, 1, 0), (7, 129, 65, 0, 1),
-                                         (130, 70, 1, 1, 1), (512, 16, 512, 1, 0), (3, 3, 0, 0, 0)])
+                                         (130, 70, 1, 1, 1), (512, 16, 512, 1, 0), (3, 3, 0, 0, 0),
+                                         # large-tile kernels (128 x 64 / 128 x 32, 3 stages)
+                                         (512, 512, 300, 0, 1), (1024, 96, 257, 0, 0),
+                                         (513, 64, 600, 1, 1), (2048, 32, 401, 0, 1),
+                                         (1537, 30, 500, 0, 0)])
 def test_grouped_dmma_gemm_matches_numpy(tg, M, N, K, ta, tb):
     r = np.random.default_rng(M * 1000 + N)
     A = r.normal(size=(K, M) if ta else (M, K))
