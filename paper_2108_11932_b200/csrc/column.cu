@@ -50,12 +50,15 @@ void column_setup(Ctx& C, const Matrix& M, int k, const DBlocks& D, ColumnSetup&
   batched_copy(C.push(cp), (int)cp.size(), C.st);
   ++C.launches;
   if (D.on()) {
+    // [D_j] V_kj for every j (Eq. 3), one launch
+    std::vector<BdItem> bi;
     for (size_t jj = 0; jj < cs.J.size(); ++jj) {
       int j = cs.J[jj], r = M.rank[M.t(k, j)];
-      bd_apply(D.d + (size_t)j * b, D.e + (size_t)j * b, D.s2 + (size_t)j * b, b,
-               cs.Wcat + (size_t)cs.seg[jj] * b, b, r, C.st);
-      ++C.launches;
+      bi.push_back({D.d + (size_t)j * b, D.e + (size_t)j * b, D.s2 + (size_t)j * b,
+                    cs.Wcat + (size_t)cs.seg[jj] * b, r});
     }
+    bd_apply_batched(C.push(bi), (int)bi.size(), b, b, C.st);
+    ++C.launches;
   }
   // Gram blocks over the suffix i >= k of each panel j
   std::vector<const double*> suf(cs.J.size(), nullptr);

@@ -776,29 +776,42 @@ void min_block_pivot(const double* d, const double* e, const uint8_t* s2, int n,
   TLRG_CUDA(cudaGetLastError());
 }
 
-// W <- D W  (dense_kernels.cpp:97-116), one thread per column
+// W <- D W  (dense_kernels.cpp:97-116): one thread per (row, column); the
+// thread of a 2x2 block's first row updates both rows (BlockDiagonal marks
+// block starts only, so the second row of a 2x2 never starts a block)
+__device__ __forceinline__ void bd_apply_row(const double* d, const double* e, const uint8_t* s2,
+                                             int n, double* x, int r) {
+  if (s2[r] && r + 1 < n) {
+    const double a = x[r], b = x[r + 1];
+    x[r] = d[r] * a + e[r] * b;
+    x[r + 1] = e[r] * a + d[r + 1] * b;
+  } else if (!(r > 0 && s2[r - 1])) {
+    x[r] *= d[r];
+  }
+}
 __global__ void bd_apply_kernel(const double* d, const double* e, const uint8_t* s2, int n,
                                 double* W, long long ld, int cols) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  double* x = W + (long long)c * ld;
-  int k = 0;
-  while (k < n) {
-    if (s2[k]) {
-      double a = x[k], b = x[k + 1];
-      x[k] = d[k] * a + e[k] * b;
-      x[k + 1] = e[k] * a + d[k + 1] * b;
-      k += 2;
-    } else {
-      x[k] *= d[k];
-      k += 1;
-    }
-  }
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int c = blockIdx.y; c < cols; c += gridDim.y) bd_apply_row(d, e, s2, n, W + (long long)c * ld, r);
 }
 void bd_apply(const double* d, const double* e, const uint8_t* s2, int n, double* W, long long ld,
               int cols, cudaStream_t st) {
-  if (cols <= 0) return;
-  bd_apply_kernel<<<(cols + 63) / 64, 64, 0, st>>>(d, e, s2, n, W, ld, cols);
+  if (cols <= 0 || n <= 0) return;
+  dim3 grid((n + 127) / 128, std::min(cols, 1024));
+  bd_apply_kernel<<<grid, 128, 0, st>>>(d, e, s2, n, W, ld, cols);
+  TLRG_CUDA(cudaGetLastError());
+}
+// one launch for a list of (D block, column block) items
+__global__ void bd_apply_batched_kernel(const BdItem* items, int n, long long ld) {
+  const BdItem it = items[blockIdx.y];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int c = 0; c < it.cols; ++c) bd_apply_row(it.d, it.e, it.s2, n, it.W + (long long)c * ld, r);
+}
+void bd_apply_batched(const BdItem* d_items, int nitems, int n, long long ld, cudaStream_t st) {
+  if (nitems <= 0 || n <= 0) return;
+  bd_apply_batched_kernel<<<dim3((n + 127) / 128, nitems), 128, 0, st>>>(d_items, n, ld);
   TLRG_CUDA(cudaGetLastError());
 }
 

@@ -262,6 +262,14 @@ void min_diag_sq(const double* L, int n, double* out, cudaStream_t st);
 void min_block_pivot(const double* d, const double* e, const uint8_t* s2, int n, double* out,
                      cudaStream_t st);
 // W <- D_j W  (block diagonal apply, rows of W)
+struct BdItem {
+  const double* d;
+  const double* e;
+  const uint8_t* s2;
+  double* W;
+  int cols;
+};
+void bd_apply_batched(const BdItem* d_items, int nitems, int n, long long ld, cudaStream_t st);
 void bd_apply(const double* d, const double* e, const uint8_t* s2, int n, double* W,
               long long ld, int cols, cudaStream_t st);
 // Schur compensation helpers
