@@ -197,7 +197,7 @@ void potrf_impl(double* A, int n, int* info, DescArena& desc, cudaStream_t st) {
 // are dropped (zero column of Rinv), so a rank-deficient sketch yields zero
 // basis columns instead of a breakdown.  One CTA, p <= 160.
 __global__ void __launch_bounds__(1024) cholqr_kernel(const double* G, int p, int n, int shift,
-                                                      double* Rinv) {
+                                                      double* Rinv, int x_in_smem) {
   extern __shared__ double csm[];
   double* R = csm;              // p x p (row-major, ld p+1)
   const int ld = p + 1;
@@ -251,24 +251,30 @@ __global__ void __launch_bounds__(1024) cholqr_kernel(const double* G, int p, in
     }
     __syncthreads();
   }
-  // R^{-1} (upper), column j by thread j (back substitution against R in smem);
-  // a dropped pivot leaves a zero row/column, i.e. a zero basis column
-  if (tid < p) {
-    const int j = tid;
-    double* x = Rinv + (long long)j * p;
-    for (int i = j + 1; i < p; ++i) x[i] = 0.0;
-    const double rjj = R[j * ld + j];
-    x[j] = rjj != 0.0 ? 1.0 / rjj : 0.0;
-    for (int i = j - 1; i >= 0; --i) {
-      const double rii = R[i * ld + i];
-      double s0 = 0.0, s1 = 0.0;
-      int l = i + 1;
-      for (; l + 1 <= j; l += 2) {
-        s0 += R[i * ld + l] * x[l];
-        s1 += R[i * ld + l + 1] * x[l + 1];
+  // R^{-1} (upper): one warp per column j, the lanes split each back-substitution
+  // sum (shared-memory column, written out at the end); a dropped pivot leaves a
+  // zero row/column, i.e. a zero basis column
+  {
+    // p x p scratch after R when it fits in shared memory, else the output itself
+    double* X = x_in_smem ? R + p * ld : Rinv;
+    const int lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    for (int j = w; j < p; j += nw) {
+      double* x = X + j * p;
+      for (int i = lane; i < p; i += 32) x[i] = 0.0;
+      __syncwarp();
+      const double rjj = R[j * ld + j];
+      if (lane == 0) x[j] = rjj != 0.0 ? 1.0 / rjj : 0.0;
+      __syncwarp();
+      for (int i = j - 1; i >= 0; --i) {
+        double s0 = 0.0;
+        for (int l = i + 1 + lane; l <= j; l += 32) s0 += R[i * ld + l] * x[l];
+        s0 = warp_sum(s0);
+        const double rii = R[i * ld + i];
+        if (lane == 0) x[i] = rii != 0.0 ? -s0 / rii : 0.0;
+        __syncwarp();
       }
-      if (l <= j) s0 += R[i * ld + l] * x[l];
-      x[i] = rii != 0.0 ? -(s0 + s1) / rii : 0.0;
+      if (x_in_smem)
+        for (int i = lane; i < p; i += 32) Rinv[(long long)j * p + i] = x[i];
     }
   }
 }
@@ -311,8 +317,13 @@ void cholqr_apply(double* Y, int n, int p, const double* Rinv, cudaStream_t st) 
 void cholqr_factor(const double* G, int p, int n, int shift, double* Rinv, cudaStream_t st) {
   static size_t lim = enable_max_dyn_smem(cholqr_kernel);
   (void)lim;
-  size_t bytes = (size_t)p * (p + 1) * 8;
-  cholqr_kernel<<<1, 1024, bytes, st>>>(G, p, n, shift, Rinv);
+  size_t bytes = ((size_t)p * (p + 1) + (size_t)p * p) * 8;  // R + R^{-1} scratch
+  int x_in_smem = 1;
+  if (bytes > lim) {
+    bytes = (size_t)p * (p + 1) * 8;
+    x_in_smem = 0;
+  }
+  cholqr_kernel<<<1, 1024, bytes, st>>>(G, p, n, shift, Rinv, x_in_smem);
   TLRG_CUDA(cudaGetLastError());
 }
 

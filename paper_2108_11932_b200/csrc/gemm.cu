@@ -106,14 +106,33 @@ static int big_config(const std::vector<GemmProblem>& probs) {
   return 0;
 }
 
-GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
+static GemmPlan plan_small(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
   int maxN = 0;
   for (auto& p : probs)
     if (p.M > 0) maxN = std::max(maxN, p.N);
+  return maxN <= 16 ? plan_grouped<64, 16>(probs, desc, st) : plan_grouped<64, 32>(probs, desc, st);
+}
+
+GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st) {
   const int big = big_config(probs);
   if (big == 1) return plan_grouped<128, 64>(probs, desc, st, 1);
   if (big == 2) return plan_grouped<128, 32>(probs, desc, st, 2);
-  return maxN <= 16 ? plan_grouped<64, 16>(probs, desc, st) : plan_grouped<64, 32>(probs, desc, st);
+  // mixed list: split off the large problems when they alone make a wave
+  std::vector<GemmProblem> large, small;
+  for (auto& p : probs) {
+    if (p.M <= 0 || p.N <= 0) continue;
+    (p.M >= 128 && p.N >= 24 ? large : small).push_back(p);
+  }
+  if (!large.empty() && !small.empty()) {
+    const int bl = big_config(large);
+    if (bl) {
+      GemmPlan P = bl == 1 ? plan_grouped<128, 64>(large, desc, st, 1)
+                           : plan_grouped<128, 32>(large, desc, st, 2);
+      P.rest = std::make_shared<GemmPlan>(plan_small(small, desc, st));
+      return P;
+    }
+  }
+  return plan_small(probs, desc, st);
 }
 
 template <int BM, int BN, int WGM, int WGN, int ST>
@@ -126,6 +145,7 @@ static void launch_big(const GemmPlan& p, cudaStream_t st) {
 }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t st) {
+  if (p.rest) gemm_launch(*p.rest, st);
   if (p.tiles == 0) return;
   if (p.big == 1)
     launch_big<128, 64, 4, 2, 3>(p, st);

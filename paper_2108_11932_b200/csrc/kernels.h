@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "gemm.cuh"
@@ -22,6 +23,9 @@ struct GemmPlan {
   const int* owner = nullptr;  // per-CTA problem index
   int n = 0, tiles = 0, bn = 32;
   int big = 0;  // 0: 64 x bn tiles; 1: 128 x 64 (8 warps); 2: 128 x 32 (4 warps)
+  // a list mixing large and small problems runs as two launches: the large
+  // ones on the large-tile kernel (this plan), the rest on the small one
+  std::shared_ptr<GemmPlan> rest;
 };
 GemmPlan gemm_plan(std::vector<GemmProblem>& probs, DescArena& desc, cudaStream_t st);
 void gemm_launch(const GemmPlan& p, cudaStream_t st);

@@ -344,74 +344,196 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
   const double tau = T.tau;
   int rep_n = 0, rep_used = 0;  // batch of projected replacement vectors
   long long rep_base = 0;
+  __shared__ int s_fast;
 
-  for (int j = 0; j < w; ++j) {
+  // deficient column j (norm below tau after its two passes): record the first
+  // tiny norm, restart from a fresh direction of the tile's own stream, project
+  // out Q and the earlier panel columns (dense_kernels.cpp:348-372); returns the
+  // norm the column is then divided by
+  auto replace_col = [&](int j, double nj) -> double {
     double* yj = Y + (long long)j * rows;
-    if (j > 0)
-      for (int pass = 0; pass < 2; ++pass) {
-        cgs_pass(Y, rows, j, S);
-        if (tid == 0)
-          for (int p = 0; p < j; ++p) Rp[p + (long long)j * w] += S.cbuf[p];
-      }
-    double nj = col_norm(yj, rows, S);
-    if (!(nj >= tau)) {
-      // deficient column: record, restart from a fresh direction of the tile's
-      // own stream, project out Q and the earlier panel columns
-      if (tid == 0 && !T.deficient[j]) {
-        T.deficient[j] = 1;
-        T.tiny[j] = isfinite(nj) ? nj : 0.0;
-      }
-      if (rep_used == rep_n) {
-        // Project the next (w - j) vectors of the tile's stream against Q in
-        // one batch: replacement vector u is stream[c0 + u*rows, ...) with
-        // y <- y - Q (Q^T y) (dense_kernels.cpp:351-358); the cursor only
-        // advances over the vectors actually consumed.
+    if (tid == 0 && !T.deficient[j]) {
+      T.deficient[j] = 1;
+      T.tiny[j] = isfinite(nj) ? nj : 0.0;
+    }
+    if (rep_used == rep_n) {
+      // Project the next (w - j) vectors of the tile's stream against Q in
+      // one batch: replacement vector u is stream[c0 + u*rows, ...) with
+      // y <- y - Q (Q^T y) (dense_kernels.cpp:351-358); the cursor only
+      // advances over the vectors actually consumed.
+      __syncthreads();
+      const long long c0 = *T.gcursor;
+      rep_base = c0;
+      rep_used = 0;
+      rep_n = w - j;
+      __syncthreads();
+      ring_copy(T.gbuf, T.gcap, c0, (long long)rows * rep_n, T.rep, PT);
+      __syncthreads();
+      if (q > 0) {
+        for (int pi = warp; pi < q * rep_n; pi += PW) {
+          const int t = pi % q, c = pi / q;
+          const double* qt = T.Q + (long long)t * rows;
+          const double* rc = T.rep + (long long)c * rows;
+          double sacc = 0.0;
+          for (int r = lane; r < rows; r += 32) sacc += qt[r] * rc[r];
+          sacc = warp_sum(sacc);
+          if (lane == 0) T.repC[t + (long long)c * q] = sacc;
+        }
         __syncthreads();
-        const long long c0 = *T.gcursor;
-        rep_base = c0;
-        rep_used = 0;
-        rep_n = w - j;
-        __syncthreads();
-        ring_copy(T.gbuf, T.gcap, c0, (long long)rows * rep_n, T.rep, PT);
-        __syncthreads();
-        if (q > 0) {
-          for (int pi = warp; pi < q * rep_n; pi += PW) {
-            const int t = pi % q, c = pi / q;
-            const double* qt = T.Q + (long long)t * rows;
-            const double* rc = T.rep + (long long)c * rows;
-            double s = 0.0;
-            for (int r = lane; r < rows; r += 32) s += qt[r] * rc[r];
-            s = warp_sum(s);
-            if (lane == 0) T.repC[t + (long long)c * q] = s;
+        for (int r = tid; r < rows; r += PT)
+          for (int c = 0; c < rep_n; ++c) {
+            double sacc = 0.0;
+            for (int t = 0; t < q; ++t)
+              sacc += T.Q[(long long)t * rows + r] * T.repC[t + (long long)c * q];
+            T.rep[r + (long long)c * rows] -= sacc;
           }
-          __syncthreads();
-          for (int r = tid; r < rows; r += PT)
-            for (int c = 0; c < rep_n; ++c) {
-              double s = 0.0;
-              for (int t = 0; t < q; ++t)
-                s += T.Q[(long long)t * rows + r] * T.repC[t + (long long)c * q];
-              T.rep[r + (long long)c * rows] -= s;
-            }
-          __syncthreads();
+        __syncthreads();
+      }
+    }
+    for (int r = tid; r < rows; r += PT) yj[r] = T.rep[r + (long long)rep_used * rows];
+    ++rep_used;
+    if (tid == 0) *T.gcursor = rep_base + (long long)rep_used * rows;
+    if (j > 0)
+      for (int pass = 0; pass < 2; ++pass) cgs_pass(Y, rows, j, S);
+    nj = col_norm(yj, rows, S);
+    if (nj == 0.0) {
+      // pathological: unit coordinate direction, written by the row's owner
+      if (tid == (j % rows) % PT) yj[j % rows] = 1.0;
+      nj = 1.0;
+    }
+    if (tid == 0) Rp[j + (long long)j * w] = 0.0;
+    return nj;
+  };
+
+  // ---- second sweep as one Gram product (see ara_fused.cu sweep2_gram): the
+  // panel is orthonormal to O(eps) after sweep 1 and the caller's BGS, so
+  // R2 = I + striu(F) + diag(F)/2 with F = Y^T Y - I, and Y <- Y R2^{-1} with
+  // R2^{-1} = I - striu(F) - diag(F)/2 (dropped terms O(|F|^2)).  Taken when no
+  // column can deflate (tau < 1/4) and |F| <= 1e-6 everywhere; otherwise the
+  // column sweep below runs.
+  bool gram_done = false;
+  if (sweep == 1 && w <= 32 && tau < 0.25) {
+    double* F = T.Rp + (long long)w * w;  // w x w scratch (the R-update buffer)
+    if (tid == 0) s_fast = 1;
+    __syncthreads();
+    for (int e = warp; e < w * (w + 1) / 2; e += PW) {
+      int jj = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+      while (jj * (jj + 1) / 2 > e) --jj;
+      while ((jj + 1) * (jj + 2) / 2 <= e) ++jj;
+      const int ii = e - jj * (jj + 1) / 2;
+      const double* xa = Y + (long long)ii * rows;
+      const double* xb = Y + (long long)jj * rows;
+      double sacc = 0.0;
+      for (int r = lane; r < rows; r += 32) sacc += xa[r] * xb[r];
+      sacc = warp_sum(sacc);
+      if (lane == 0) {
+        const double f = sacc - (ii == jj ? 1.0 : 0.0);
+        F[ii + (long long)jj * w] = f;
+        if (!(fabs(f) <= 1e-6)) s_fast = 0;
+      }
+    }
+    __syncthreads();
+    if (s_fast) {
+      for (long long e = tid; e < (long long)w * w; e += PT) {
+        const int ii = (int)(e % w), jj = (int)(e / w);
+        const double f = ii <= jj ? F[ii + (long long)jj * w] : 0.0;
+        Rp[e] = ii < jj ? f : ii == jj ? 1.0 + 0.5 * f : 0.0;
+      }
+      // y_row <- y_row R2^{-1}, one row per thread
+      for (int r = tid; r < rows; r += PT) {
+        double yr[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) yr[c] = c < w ? Y[r + (long long)c * rows] : 0.0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          if (c < w) {
+            double v = yr[c] * (1.0 - 0.5 * F[c + (long long)c * w]);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < c) v -= yr[i] * F[i + (long long)c * w];
+            Y[r + (long long)c * rows] = v;
+          }
         }
       }
-      for (int r = tid; r < rows; r += PT) yj[r] = T.rep[r + (long long)rep_used * rows];
-      ++rep_used;
-      if (tid == 0) *T.gcursor = rep_base + (long long)rep_used * rows;
-      if (j > 0)
-        for (int pass = 0; pass < 2; ++pass) cgs_pass(Y, rows, j, S);
-      nj = col_norm(yj, rows, S);
-      if (nj == 0.0) {
-        // pathological: unit coordinate direction, written by the row's owner
-        if (tid == (j % rows) % PT) yj[j % rows] = 1.0;
-        nj = 1.0;
-      }
-      if (tid == 0) Rp[j + (long long)j * w] = 0.0;
-    } else {
-      if (tid == 0) Rp[j + (long long)j * w] = nj;
+      __syncthreads();
+      gram_done = true;
     }
+  }
+
+  // ---- column sweep: two-pass Gram-Schmidt with ONE block reduction per
+  // column (delayed second pass; see ara_fused.cu dcgs_step).  Step s
+  // finalizes column s-1 and runs the first pass of column s:
+  //   a = Y_{<s-1}^T v, d = v^T v, b = Y_{<s-1}^T y_s, c = v^T y_s
+  //   v <- v - Y a, n^2 = d - |a|^2, u = v / n
+  //   y_s <- y_s - Y_{<s-1} b - u (c - a^T b) / n
+  for (int st = 1; st <= w && !gram_done; ++st) {
+    const int JA = st - 1;
+    const bool hasb = st < w;
+    double* v = Y + (long long)JA * rows;
+    double* ys = hasb ? Y + (long long)st * rows : nullptr;
+    const int nd = hasb ? 2 * JA + 2 : JA + 1;
+    __syncthreads();
+    for (int t = warp; t < nd; t += PW) {
+      const double *xa, *xb;
+      if (t < JA) {
+        xa = Y + (long long)t * rows;
+        xb = v;
+      } else if (t == JA) {
+        xa = v;
+        xb = v;
+      } else if (t < 2 * JA + 1) {
+        xa = Y + (long long)(t - JA - 1) * rows;
+        xb = ys;
+      } else {
+        xa = v;
+        xb = ys;
+      }
+      double sacc = 0.0;
+      for (int r = lane; r < rows; r += 32) sacc += xa[r] * xb[r];
+      sacc = warp_sum(sacc);
+      if (lane == 0) S.cbuf[t] = sacc;
+    }
+    __syncthreads();
+    const double* cf = S.cbuf;
+    double asq = 0.0;
+    for (int p = 0; p < JA; ++p) asq += cf[p] * cf[p];
+    const double nj = sqrt(fmax(cf[JA] - asq, 0.0));
+    if (tid == 0)
+      for (int p = 0; p < JA; ++p) Rp[p + (long long)JA * w] += cf[p];
+    if (!(nj >= tau)) {
+      const double nr = replace_col(JA, nj);
+      const double inv = 1.0 / nr;
+      for (int r = tid; r < rows; r += PT) v[r] *= inv;
+      if (hasb) {
+        cgs_pass(Y, rows, st, S);  // first pass of column s against the final columns
+        if (tid == 0)
+          for (int p = 0; p < st; ++p) Rp[p + (long long)st * w] += S.cbuf[p];
+      }
+      continue;
+    }
+    if (tid == 0) Rp[JA + (long long)JA * w] = nj;
     const double inv = 1.0 / nj;
-    for (int r = tid; r < rows; r += PT) yj[r] *= inv;
+    double beta = 0.0;
+    if (hasb) {
+      double ab = 0.0;
+      for (int p = 0; p < JA; ++p) ab += cf[p] * cf[JA + 1 + p];
+      beta = (cf[2 * JA + 1] - ab) * inv;
+      if (tid == 0) {
+        for (int p = 0; p < JA; ++p) Rp[p + (long long)st * w] += cf[JA + 1 + p];
+        Rp[JA + (long long)st * w] += beta;
+      }
+    }
+    for (int r = tid; r < rows; r += PT) {
+      double sa = 0.0, sb = 0.0;
+      for (int p = 0; p < JA; ++p) {
+        const double yv = Y[(long long)p * rows + r];
+        sa += cf[p] * yv;
+        if (hasb) sb += cf[JA + 1 + p] * yv;
+      }
+      const double u = (v[r] - sa) * inv;
+      v[r] = u;
+      if (hasb) ys[r] -= sb + beta * u;
+    }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
   __syncthreads();
@@ -502,7 +624,7 @@ void panel_mgs(PanelTask* d_tasks, int ntask, int sweep, int finalize, int max_w
   static size_t lim = enable_max_dyn_smem(panel_mgs_kernel);
   if (ntask <= 0) return;
   int part_len = max_width;
-  int cbuf_len = max_width > max_rows ? max_width : max_rows;
+  int cbuf_len = std::max(2 * max_width + 2, max_rows);  // DCGS2 dot list <= 2 w + 2
   size_t base = ((size_t)2 * PW * part_len + cbuf_len + MT_N) * 8;
   size_t rp = (size_t)max_width * max_width * 8;
   size_t ys = (size_t)max_rows * max_width * 8;
