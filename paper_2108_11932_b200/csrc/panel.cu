@@ -380,13 +380,26 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
           if (lane == 0) T.repC[t + (long long)c * q] = sacc;
         }
         __syncthreads();
-        for (int r = tid; r < rows; r += PT)
-          for (int c = 0; c < rep_n; ++c) {
-            double sacc = 0.0;
-            for (int t = 0; t < q; ++t)
-              sacc += T.Q[(long long)t * rows + r] * T.repC[t + (long long)c * q];
-            T.rep[r + (long long)c * rows] -= sacc;
+        // rep -= Q (Q^T rep): each Q element is loaded once per row and
+        // applied to up to 16 replacement vectors held in registers
+        for (int c0 = 0; c0 < rep_n; c0 += 16) {
+          const int nc = min(16, rep_n - c0);
+          for (int r = tid; r < rows; r += PT) {
+            double acc[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+            for (int t = 0; t < q; ++t) {
+              const double qv = T.Q[(long long)t * rows + r];
+              const double* rc = T.repC + t + (long long)c0 * q;
+#pragma unroll
+              for (int c = 0; c < 16; ++c)
+                if (c < nc) acc[c] += qv * rc[(long long)c * q];
+            }
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c < nc) T.rep[r + (long long)(c0 + c) * rows] -= acc[c];
           }
+        }
         __syncthreads();
       }
     }
