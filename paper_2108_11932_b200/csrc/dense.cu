@@ -833,6 +833,17 @@ __global__ void frob_sq_kernel(const double* p, long long n, double* out) {
   s = block_sum(s, red);
   if (threadIdx.x == 0) *out = s;
 }
+__global__ void vec_sum_kernel(const double* p, int n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) s += p[t];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+void block_sum_device(const double* p, int n, double* out, cudaStream_t st) {
+  vec_sum_kernel<<<1, 256, 0, st>>>(p, n, out);
+  TLRG_CUDA(cudaGetLastError());
+}
 void frob_sq(const double* p, long long n, double* out, cudaStream_t st) {
   frob_sq_kernel<<<1, 1024, 0, st>>>(p, n, out);
   TLRG_CUDA(cudaGetLastError());
@@ -863,21 +874,37 @@ void fill_gaussian_philox(double* out, long long n, uint64_t seed, cudaStream_t 
 
 // corr[i] = sum_j |D_ij - (Xl Xr^T)_ij| is computed after the GEMM R = D - Xl Xr^T;
 // this kernel takes R directly.
-__global__ void rowsum_abs_kernel(const double* R, int n, double* corr, double* frob_part) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// corr_i = sum_j |R_ij| and the row's sum of squares: a CTA owns 32 rows, its
+// 16 thread groups split the columns, partials combined in a fixed order
+constexpr int RS_G = 16;
+__global__ void __launch_bounds__(32 * RS_G) rowsum_abs_kernel(const double* R, int n, double* corr,
+                                                               double* frob_part) {
+  __shared__ double ps[RS_G][32], pf[RS_G][32];
+  const int r = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + r;
   double s = 0.0, f = 0.0;
-  for (int j = 0; j < n; ++j) {
-    double v = R[i + (long long)j * n];
-    s += fabs(v);
-    f += v * v;
+  if (i < n)
+    for (int j = g; j < n; j += RS_G) {
+      const double v = R[i + (long long)j * n];
+      s += fabs(v);
+      f += v * v;
+    }
+  ps[g][r] = s;
+  pf[g][r] = f;
+  __syncthreads();
+  if (g == 0 && i < n) {
+    double a = 0.0, b = 0.0;
+    for (int t = 0; t < RS_G; ++t) {
+      a += ps[t][r];
+      b += pf[t][r];
+    }
+    corr[i] = a;
+    frob_part[i] = b;
   }
-  corr[i] = s;
-  frob_part[i] = f;
 }
 void rowsum_abs_residual(const double* R, const double*, const double*, int n, int,
                          double* corr, double* frob_part, cudaStream_t st) {
-  rowsum_abs_kernel<<<(n + 127) / 128, 128, 0, st>>>(R, n, corr, frob_part);
+  rowsum_abs_kernel<<<(n + 31) / 32, 32 * RS_G, 0, st>>>(R, n, corr, frob_part);
   TLRG_CUDA(cudaGetLastError());
 }
 

@@ -460,7 +460,7 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
     C.gemm(p2);
   }
   rowsum_abs_residual(Rm, nullptr, nullptr, n, 0, corr, fp, C.st);
-  frob_sq(Rm, (long long)n * n, frob, C.st);  // ||R||_F^2
+  block_sum_device(fp, n, frob, C.st);  // ||R||_F^2 from the per-row sums of squares
   C.launches += 2;
 }
 

@@ -285,5 +285,7 @@ void fill_gaussian_philox(double* out, long long n, uint64_t seed, cudaStream_t 
 // generic elementwise
 void fill_zero(double* p, long long n, cudaStream_t st);
 void frob_sq(const double* p, long long n, double* out, cudaStream_t st);
+// *out = sum of n values (one CTA, fixed order)
+void block_sum_device(const double* p, int n, double* out, cudaStream_t st);
 
 }  // namespace tlrg

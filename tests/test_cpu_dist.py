@@ -57,3 +57,28 @@ def test_nccl_id_broadcast_and_allmax_over_gloo():
     assert set(got) == {0, 1}
     assert got[0][0] == got[1][0] and len(got[0][0]) == 128
     assert got[0][1] == got[1][1] == 2.0
+
+
+def test_bench_torchrun_contract_reference_arm_world2():
+    """bench.py launched the way the driver launches N > 1 (torch.distributed.run,
+    two ranks, 127.0.0.1): rank 0 alone runs the reference arm and prints ONE
+    JSON line, the other rank exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1", TLRG_REF_BUDGET_S="60")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--impl", "reference", "--config", "cfg1", "--gpus", "2", "--steps", "1",
+           "--warmup", "0"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "s" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "reference"

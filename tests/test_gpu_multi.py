@@ -79,3 +79,65 @@ def test_split_column_ldlt_is_bitwise_identical(tg, ref):
             (Da, pa), (Db, pb) = F.dblock(k), F1.dblock(k)
             assert np.array_equal(pa, pb)
             assert np.array_equal(Da.d, Db.d) and np.array_equal(Da.e, Db.e)
+
+
+def _nccl_worker(rank, world, port, parts, meta, q):
+    """One process per GPU: the NCCL transport of the column exchange."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    import paper_2108_11932_b200 as tg
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        ctx = tg.Context(rank)
+        obj = [tg.tlr.nccl_unique_id(ctx) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.attach_nccl(rank, world, obj[0])
+        n, b, eps, bs, seed = meta
+        diag, ranks, U, V = parts
+        A = tg.TlrMatrix.from_parts(n, b, eps, diag, ranks, U, V, ctx=ctx)
+        F = tg.tlr_cholesky(A, tg.AraConfig(block_samples=bs, eps=eps, seed=seed))
+        q.put((rank, F.L.ranks().tolist(), F.L.to_parts()[0][-1].tolist()))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # reported to the parent
+        q.put((rank, "error", repr(e)))
+
+
+def test_nccl_two_processes_bitwise_equal_to_one_gpu(tg, ref):
+    """Two processes, one GPU each, NCCL panel exchange (comm.cu): the factor
+    equals the single-GPU factor bit for bit.  Needs two visible GPUs."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two visible GPUs")
+    n, b, eps, bs, seed = 2048, 128, 1e-6, 16, 5
+    A_ref = covariance_ref(ref, n, b, eps)
+    parts = A_ref.to_parts()
+    one = tg.tlr_cholesky(tg.TlrMatrix.from_parts(n, b, eps, *parts),
+                          tg.AraConfig(block_samples=bs, eps=eps, seed=seed))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, parts, (n, b, eps, bs, seed), q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        item = q.get(timeout=600)
+        got[item[0]] = item[1:]
+    for p in procs:
+        p.join(120)
+    for r in (0, 1):
+        assert got[r][0] != "error", got[r]
+        assert got[r][0] == one.L.ranks().tolist()
+        assert np.array_equal(np.array(got[r][1]), one.L.to_parts()[0][-1])
