@@ -207,10 +207,10 @@ __device__ __forceinline__ void cp_async_wait_n() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int BM, int BN, int WGM, int WGN, int STAGES>
+template <int BM, int BN, int WGM, int WGN, int STAGES, int BK = 16>
 __global__ void __launch_bounds__(32 * WGM * WGN) grouped_gemm_big_kernel(
     const GemmProblem* __restrict__ probs, const int* __restrict__ owner) {
-  constexpr int NT = 32 * WGM * WGN, BK = 16, SA = BM + 4, SB = BN + 4;
+  constexpr int NT = 32 * WGM * WGN, SA = BM + 4, SB = BN + 4;
   constexpr int WM = BM / WGM, WN = BN / WGN, FM = WM / 8, FN = WN / 8;
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                        // STAGES x BK x SA
