@@ -585,8 +585,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     roff[s] = rtot;
     rtot += (long long)q[s] * q[s];
   }
-  double *Rr = nullptr, *Vs = nullptr, *RtAp = nullptr;
-  std::vector<int> kstar_of(T, -1);  // truncated-core width per tile (-1: full core)
+  double *Rr = nullptr, *Vs = nullptr;
   if (recomp && qmax > 0) {
     Rr = C.buf<double>("Rr", (size_t)rtot + 1);
     double* Rpr = C.buf<double>("Rpr", (size_t)2 * rtot + 1);
@@ -652,44 +651,14 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     panel_tau(d_tasks, (int)tasks.size(), C.st);
     panel_mgs(d_tasks, (int)tasks.size(), 0, 0, qmax, cols, C.st);
     panel_mgs(d_tasks, (int)tasks.size(), 1, 1, qmax, cols, C.st);
-    C.launches += 3;
-    // truncated core: rows of R whose tail norm is below 1e-3 cut cannot move a
-    // singular value across the cut; the SVD runs on R(0:k*, :)^T (q x k*)
-    // (see rtrunc_kernel).  Only for cores wide enough to pay off.
-    const double thr = 1e-3 * cut;
-    int* kst = C.buf<int>("kstar", (size_t)T);
-    double* RtA = C.buf<double>("RtA", (size_t)rtot + 1);
-    RtAp = RtA;
-    std::vector<RtruncTask> rt;
-    for (int s : sl) rt.push_back({Rr + roff[s], RtA + roff[s], q[s], kst + s});
-    const bool trunc = qmax > 64 && qmax <= 512;
-    std::vector<int> hk(T, 0);
-    int kmax = 0;
-    if (trunc) {
-      rtrunc(C.push(rt), (int)rt.size(), thr, C.st);
-      ++C.launches;
-      TLRG_CUDA(cudaMemcpyAsync(hk.data(), kst, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
-      C.wait();
-      for (size_t t = 0; t < sl.size(); ++t) {
-        const int s = sl[t];
-        svd[t].A = RtA + roff[s];
-        svd[t].m = q[s];
-        svd[t].n = hk[s];
-        kmax = std::max(kmax, hk[s]);
-      }
-    }
-    SvdTask* d_svd = C.push(svd);
-    jacobi_svd(d_svd, (int)svd.size(), trunc ? std::max(kmax, 1) : qmax, C.st, qmax);
-    if (trunc) svd_swap_scale(d_svd, (int)svd.size(), C.st);
-    C.launches += trunc ? 2 : 1;
+    jacobi_svd(C.push(svd), (int)svd.size(), qmax, C.st);
+    C.launches += 4;
     h2 = hnow();
     std::vector<int> hr(T);
     TLRG_CUDA(cudaMemcpyAsync(hr.data(), rko, sizeof(int) * T, cudaMemcpyDeviceToHost, C.st));
     C.wait();
     h3 = hnow();
     for (int s : sl) fr[s] = hr[s];
-    if (trunc)
-      for (int s : sl) kstar_of[s] = hk[s];
   } else {
     for (int s = 0; s < T; ++s) fr[s] = q[s];
   }
@@ -723,22 +692,6 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       cpy.push_back({Uo + (size_t)s * maxrows * FUSED_QMAX, out.U[s], S.rows[s], S.rows[s],
                      S.rows[s], fr[s]});
       cpy.push_back({Vo + (size_t)s * cols * FUSED_QMAX, out.V[s], cols, cols, cols, fr[s]});
-    } else if (recomp && kstar_of[s] >= 0) {
-      // truncated core A = R_k^T = U' S V'^T: V_s = U' (scaled in place, q x r),
-      // U_s S = V' S (k* x r):  Q <- Q V_s ;  B <- Z(:, 0:k*) (V' S)
-      const int ks = kstar_of[s];
-      GemmProblem g{};
-      g.A = Q + s * Qstride; g.lda = S.rows[s];
-      g.B = RtAp + roff[s]; g.ldb = q[s];
-      g.C = out.U[s]; g.ldc = S.rows[s];
-      g.M = S.rows[s]; g.N = fr[s]; g.K = q[s]; g.alpha = 1.0;
-      pu.push_back(g);
-      GemmProblem h{};
-      h.A = Bb + boff[s]; h.lda = cols;
-      h.B = Vs + roff[s]; h.ldb = std::max(ks, 1);
-      h.C = out.V[s]; h.ldc = cols;
-      h.M = cols; h.N = fr[s]; h.K = ks; h.alpha = 1.0;
-      pu.push_back(h);
     } else if (recomp) {
       // Q <- Q V_s ;  B <- Z (U_s sigma)
       GemmProblem g{};

@@ -150,15 +150,6 @@ struct SvdTask {
   double tol;   // rotation threshold (0 = rounding level m * eps_mach)
 };
 void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m = 0);
-// recompression core truncation (q <= 512): k* and A = R(0:k*, :)^T, see ortho.cu
-struct RtruncTask {
-  const double* R;
-  double* A;
-  int q;
-  int* kstar;
-};
-void rtrunc(const RtruncTask* d_tasks, int ntask, double thr, cudaStream_t st);
-void svd_swap_scale(SvdTask* d_tasks, int ntask, cudaStream_t st);
 // symmetric (PSD) core: A <- V diag(lam), V, |lam| sorted descending (n <= 160)
 void sym_jacobi(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st);
 

@@ -167,68 +167,6 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   if (tid == 0) *T.rank_out = cnt;
 }
 
-// ------------------------------------------ TRUNCATED CORE (recompression) --
-// R (q x q upper triangular from orthog) -> k* = the smallest k with
-// ||R(k:q, :)||_F <= thr, and A = R(0:k*, :)^T (q x k*, ld q).  Rows below k*
-// move every singular value of R by at most thr (Weyl), so with thr far below
-// the recompression cut the truncation decisions and the kept triplets are
-// those of R; the SVD then costs O(q k*^2) per sweep instead of O(q^3).
-__global__ void __launch_bounds__(256) rtrunc_kernel(const RtruncTask* tasks, double thr) {
-  __shared__ double rowsq[512];
-  __shared__ int s_k;
-  const RtruncTask t = tasks[blockIdx.x];
-  const double* R = t.R;
-  double* A = t.A;
-  const int q = t.q;
-  int* kstar = t.kstar;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < q; i += 256) {
-    double s = 0.0;
-    for (int j = i; j < q; ++j) s += R[i + (long long)j * q] * R[i + (long long)j * q];
-    rowsq[i] = s;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    int k = q;
-    for (int i = q - 1; i >= 0; --i) {
-      t += rowsq[i];
-      if (t > thr * thr) break;
-      k = i;
-    }
-    s_k = k;
-    *kstar = k;
-  }
-  __syncthreads();
-  const int k = s_k;
-  for (long long e = tid; e < (long long)q * k; e += 256) {
-    const int r = (int)(e % q), c = (int)(e / q);
-    A[e] = r >= c ? R[c + (long long)r * q] : 0.0;  // A(r, c) = R(c, r)
-  }
-}
-void rtrunc(const RtruncTask* d_tasks, int ntask, double thr, cudaStream_t st) {
-  if (ntask <= 0) return;
-  rtrunc_kernel<<<ntask, 256, 0, st>>>(d_tasks, thr);
-  TLRG_CUDA(cudaGetLastError());
-}
-// after the Jacobi SVD of A = R_k^T (A V' = U' S, sorted): A <- U' (columns
-// divided by sigma), V <- V' S  -- the right singular vectors of R and the
-// scaled left ones, the operands of Q V_s and Z U_s S
-__global__ void svd_swap_scale_kernel(SvdTask* tasks) {
-  SvdTask& T = tasks[blockIdx.x];
-  const int n = T.n, m = T.m > 0 ? T.m : T.n;
-  for (long long e = threadIdx.x; e < (long long)m * n; e += blockDim.x) {
-    const double s = T.sig[e / m];
-    T.A[e] = s > 0.0 ? T.A[e] / s : 0.0;
-  }
-  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) T.V[e] *= T.sig[e / n];
-}
-void svd_swap_scale(SvdTask* d_tasks, int ntask, cudaStream_t st) {
-  if (ntask <= 0) return;
-  svd_swap_scale_kernel<<<ntask, 256, 0, st>>>(d_tasks);
-  TLRG_CUDA(cudaGetLastError());
-}
-
 // ------------------------------------------- ONE-SIDED JACOBI (small) ------
 // Same algorithm and output as jacobi_svd for cores n <= 64 held in shared
 // memory, but instruction-lean: 256 threads, EIGHT lanes per column pair (4
