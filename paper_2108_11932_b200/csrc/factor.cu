@@ -377,7 +377,10 @@ bool modified_cholesky_device(Ctx& C, double* A, int n) {
 // consumed on the device (GEMM K from *rank), so the whole step enqueues without
 // a host round trip; the caller checks afterwards that at least 8 directions of
 // slack remained (r <= p - 8) and re-runs with a wider sketch otherwise.
-constexpr int kSchurMaxWidth = 160;  // sketch width cap (shared-memory Cholesky-QR)
+// sketch width cap: the p x p core's two-sided Jacobi keeps B and V in shared
+// memory up to p = 112 (the one-sided fallback in global memory was ~10x slower
+// at p = 160); wider eps-ranks go through the chunked spectrum split
+constexpr int kSchurMaxWidth = 112;
 int schur_comp_width(int n, int rank_hint) {
   int p = std::max(24, rank_hint + 16);
   p = ((p + 7) / 8) * 8;
@@ -435,7 +438,7 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
   sv[0].n = p; sv[0].cut = eps;
   sv[0].tol = 1e-14;  // off-diagonals below 1e-14 ||B||_F: ample for the eps-level split
   // symmetric PSD core: two-sided Jacobi (no dot products; 3 barriers a step)
-  if (p <= 64) sym_jacobi(C.push(sv), 1, p, C.st);
+  if (p <= kSchurMaxWidth) sym_jacobi(C.push(sv), 1, p, C.st);
   else jacobi_svd(C.push(sv), 1, p, C.st);
   ++C.launches;
   // R = D - (Q A_B)(Q V_B)^T restricted to the r = *rank_out retained directions
