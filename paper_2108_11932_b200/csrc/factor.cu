@@ -388,7 +388,7 @@ int schur_comp_width(int n, int rank_hint) {
   return p > n ? n : p;
 }
 void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t seed, int p,
-                        int attempt, double* corr, double* frob, int* rank_out) {
+                        int attempt, double* corr, double* frob, int* rank_out, int power) {
   double* Om = C.buf<double>("sc_Om", (size_t)n * p);
   double* Y = C.buf<double>("sc_Y", (size_t)n * p);
   double* Bm = C.buf<double>("sc_B", (size_t)p * p);
@@ -422,8 +422,11 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
   };
   DtimesX(Om, Y);
   orth(Y);
-  DtimesX(Y, Om);  // power iteration
-  orth(Om);
+  for (int it = 0; it < power; ++it) {  // power iterations
+    DtimesX(Y, Om);
+    orth(Om);
+    if (it + 1 < power) std::swap(Y, Om);
+  }
   DtimesX(Om, Y);  // Y = D Q
   {
     std::vector<GemmProblem> pr(1);
@@ -469,9 +472,9 @@ void schur_comp_enqueue(Ctx& C, const double* Dk, int n, double eps, uint64_t se
 
 // synchronous form: widen the sketch until the slack test holds; when the
 // eps-rank of D exceeds what one sketch can hold (kSchurMaxWidth - 8; measured
-// 82-278 at m = 1024, eps = 1e-3), split the spectrum in chunks: the top p - 16
-// Ritz pairs of each full-width sketch (16 directions of oversampling plus a
-// power step behind them) are deflated from a working copy of D, and the next
+// 82-278 at m = 1024, eps = 1e-3), split the spectrum in chunks: the top p - 32
+// Ritz pairs of each full-width sketch (32 directions of oversampling plus two
+// power steps behind them) are deflated from a working copy of D, and the next
 // sketch runs on the deflated matrix, until one has slack.  R = D - kept parts
 // is then the last chunk's residual.
 void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint64_t seed,
@@ -483,7 +486,9 @@ void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint
   double* Dwork = nullptr;
   int deflated = 0;
   for (int attempt = 0;; ++attempt) {
-    schur_comp_enqueue(C, Dw, n, eps, seed, p, attempt, corr, frob, rk);
+    // a full-width sketch (the chunked split deflates its Ritz pairs) takes a
+    // second power step: the deflated pairs' errors add up in rowsum |R|
+    schur_comp_enqueue(C, Dw, n, eps, seed, p, attempt, corr, frob, rk, p >= cap ? 2 : 1);
     int* h = C.pinned_ints(1);
     TLRG_CUDA(cudaMemcpyAsync(h, rk, sizeof(int), cudaMemcpyDeviceToHost, C.st));
     C.wait();
@@ -495,13 +500,13 @@ void schur_compensation_device(Ctx& C, const double* Dk, int n, double eps, uint
       p = std::min(cap, 2 * p);
       continue;
     }
-    // full-width sketch without slack: deflate its top p - 16 Ritz pairs
+    // full-width sketch without slack: deflate its top p - 32 Ritz pairs
     if (!Dwork) {
       Dwork = C.buf<double>("sc_Dwork", (size_t)n * n);
       dcopy(Dk, Dwork, (long long)n * n, C.st);
       Dw = Dwork;
     }
-    const int kd = p - 16;
+    const int kd = p - 32;  // 32 directions of oversampling behind the deflated pairs
     std::vector<GemmProblem> pr(1);
     pr[0] = GemmProblem{};
     pr[0].A = C.buf<double>("sc_Xl", (size_t)n * p); pr[0].lda = n;
@@ -796,7 +801,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
         cudaEventRecord(de1.e, C.st);
         if (comp)
           schur_comp_enqueue(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), p_comp, 0,
-                             corr, frob, info + 2);
+                             corr, frob, info + 2, p_comp >= std::min(rk, kSchurMaxWidth) ? 2 : 1);
         cudaEventRecord(de2.e, C.st);
         diag_tail();
         diag_inverse();
