@@ -651,7 +651,22 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     panel_tau(d_tasks, (int)tasks.size(), C.st);
     panel_mgs(d_tasks, (int)tasks.size(), 0, 0, qmax, cols, C.st);
     panel_mgs(d_tasks, (int)tasks.size(), 1, 1, qmax, cols, C.st);
-    jacobi_svd(C.push(svd), (int)svd.size(), qmax, C.st);
+    {
+      // cores wider than the shared-memory Jacobi get a thread-block cluster
+      // each (same result); they go first, the narrow rest follows
+      const int nst = jacobi_staged_max_n();
+      std::stable_sort(svd.begin(), svd.end(),
+                       [](const SvdTask& a, const SvdTask& b) { return a.n > b.n; });
+      int nwide = 0;
+      while (nwide < (int)svd.size() && svd[nwide].n > nst && svd[nwide].n <= 512) ++nwide;
+      SvdTask* d_svd = C.push(svd);
+      if (nwide) {
+        jacobi_svd_wide(d_svd, nwide, svd[0].n, C.st);
+        ++C.launches;
+      }
+      if (nwide < (int)svd.size()) jacobi_svd(d_svd + nwide, (int)svd.size() - nwide,
+                                              svd[nwide].n, C.st);
+    }
     C.launches += 4;
     h2 = hnow();
     std::vector<int> hr(T);

@@ -303,6 +303,191 @@ void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max
   TLRG_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------- ONE-SIDED JACOBI (wide) ------
+// The same one-sided Jacobi (same pair schedule, rotation rule, tolerances and
+// output order as jacobi_svd_kernel, so the result is bitwise identical) for
+// cores too wide for shared memory (n > ~118, A and V in L2).  One task per
+// thread-block cluster of JW_CL CTAs: the n/2 disjoint pairs of a step are
+// spread over all JW_CL * 16 warps of the cluster, a cluster barrier
+// (release/acquire) separates the steps, and each warp keeps its two columns
+// in registers between the dot products and the rotation (one L2 round trip
+// per column instead of two, and no serial pair loop per warp).  At cfg4's
+// recompression (q-hat up to 276) this is the column's critical path.
+constexpr int JW_T = 512, JW_CL = 8;
+
+template <int E>
+__global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
+  const int crank = (int)cluster_ctarank();
+  SvdTask& T = tasks[blockIdx.x / JW_CL];
+  const int n = T.n, m = T.m > 0 ? T.m : T.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = JW_T / 32;
+  const int gw = crank * nw + warp, gnw = JW_CL * nw, gtid = crank * JW_T + tid;
+  __shared__ int s_rot[2];
+  __shared__ double red[32];
+  __shared__ int cnt;
+  if (tid == 0) cnt = 0;
+  if (n == 0) {
+    if (crank == 0 && tid == 0) *T.rank_out = 0;
+    return;
+  }
+  double* A = T.work;                  // m x n
+  double* V = A + (long long)m * n;    // n x n
+  for (long long e = gtid; e < (long long)m * n; e += JW_CL * JW_T) __stcg(A + e, T.A[e]);
+  for (long long e = gtid; e < (long long)n * n; e += JW_CL * JW_T)
+    __stcg(V + e, (e % n == e / n) ? 1.0 : 0.0);
+  if (tid == 0) s_rot[0] = s_rot[1] = 0;
+  double f = 0.0;  // every CTA forms the same Frobenius norm (same order as the 1-CTA kernel)
+  {
+    // the 1-CTA kernel reduces with 1024 threads: reproduce its partition
+    double p0 = 0.0, p1 = 0.0;
+    for (long long e = tid; e < (long long)m * n; e += 1024) p0 += T.A[e] * T.A[e];
+    for (long long e = tid + 512; e < (long long)m * n; e += 1024) p1 += T.A[e] * T.A[e];
+    p0 = warp_sum(p0);
+    p1 = warp_sum(p1);
+    if (lane == 0) {
+      red[warp] = p0;
+      red[warp + 16] = p1;
+    }
+    __syncthreads();
+    for (int i = 0; i < 32; ++i) f += red[i];
+  }
+  const double tiny2 = f * 1e-34;
+  const double tol = T.tol > 0.0 ? T.tol : fmax(1e-15, (double)m * 2.220446049250313e-16);
+  const int nn = n + (n & 1);
+  int* rot0 = static_cast<int*>(__cluster_map_shared_rank(s_rot, 0));
+  int* cnt0 = static_cast<int*>(__cluster_map_shared_rank(&cnt, 0));
+  cluster_sync_all();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    for (int step = 0; step < nn - 1; ++step) {
+      for (int pi = gw; pi < nn / 2; pi += gnw) {
+        int p = (step + pi) % (nn - 1);
+        int q = pi == 0 ? nn - 1 : (step - pi + nn - 1) % (nn - 1);
+        if (p >= n || q >= n) continue;
+        double* ap = A + (long long)p * m;
+        double* aq = A + (long long)q * m;
+        double x[E], y[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int r = lane + 32 * e;
+          x[e] = r < m ? __ldcg(ap + r) : 0.0;
+          y[e] = r < m ? __ldcg(aq + r) : 0.0;
+        }
+        double al = 0, be = 0, ga = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          al += x[e] * x[e];
+          be += y[e] * y[e];
+          ga += x[e] * y[e];
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (al > tiny2 && be > tiny2 && ga * ga > tol * tol * (al * be)) {
+          const double dl = be - al;
+          double t = (dl >= 0 ? 2.0 * ga : -2.0 * ga) / (fabs(dl) + sqrt(dl * dl + 4.0 * ga * ga));
+          double c = rsqrt(1.0 + t * t), s = c * t;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < m) {
+              __stcg(ap + r, c * x[e] - s * y[e]);
+              __stcg(aq + r, s * x[e] + c * y[e]);
+            }
+          }
+          double* vp = V + (long long)p * n;
+          double* vq = V + (long long)q * n;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            x[e] = r < n ? __ldcg(vp + r) : 0.0;
+            y[e] = r < n ? __ldcg(vq + r) : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < n) {
+              __stcg(vp + r, c * x[e] - s * y[e]);
+              __stcg(vq + r, s * x[e] + c * y[e]);
+            }
+          }
+          if (lane == 0) atomicOr(rot0 + (sweep & 1), 1);
+        }
+      }
+      cluster_sync_all();
+      // the other parity's flag was read by every CTA before this barrier
+      if (step == 0 && crank == 0 && tid == 0) s_rot[(sweep + 1) & 1] = 0;
+    }
+    if (!*reinterpret_cast<volatile int*>(rot0 + (sweep & 1))) break;
+  }
+  // singular values = column norms of A; then the sorted write-back
+  for (int p = gw; p < n; p += gnw) {
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s += __ldcg(A + (long long)p * m + r) * __ldcg(A + (long long)p * m + r);
+    s = warp_sum(s);
+    if (lane == 0) __stcg(T.sig + p, sqrt(s));
+  }
+  cluster_sync_all();
+  for (int p = gw; p < n; p += gnw) {
+    double sp = __ldcg(T.sig + p);
+    int rk = 0;
+    for (int q = lane; q < n; q += 32) {
+      double sq = __ldcg(T.sig + q);
+      rk += (sq > sp || (sq == sp && q < p)) ? 1 : 0;
+    }
+    rk = warp_sum_int(rk);
+    if (lane == 0 && sp > T.cut) atomicAdd(cnt0, 1);
+    for (int r = lane; r < m; r += 32)
+      __stcg(T.A + (long long)rk * m + r, __ldcg(A + (long long)p * m + r));
+    for (int r = lane; r < n; r += 32)
+      __stcg(T.V + (long long)rk * n + r, __ldcg(V + (long long)p * n + r));
+  }
+  cluster_sync_all();
+  // sigma in descending order
+  for (int p = gw; p < n; p += gnw) {
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) {
+      const double v = __ldcg(T.A + (long long)p * m + r);
+      s += v * v;
+    }
+    s = warp_sum(s);
+    if (lane == 0) T.sig[p] = sqrt(s);
+  }
+  if (crank == 0 && tid == 0) *T.rank_out = cnt;
+  cluster_sync_all();  // no CTA leaves while its shared memory may still be addressed
+}
+
+void jacobi_svd_wide(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st) {
+  if (ntask <= 0) return;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)(ntask * JW_CL));
+  lc.blockDim = dim3(JW_T);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = JW_CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  if (max_n <= 256)
+    TLRG_CUDA(cudaLaunchKernelEx(&lc, jacobi_wide_kernel<8>, d_tasks));
+  else if (max_n <= 512)
+    TLRG_CUDA(cudaLaunchKernelEx(&lc, jacobi_wide_kernel<16>, d_tasks));
+  else
+    throw CudaError("jacobi_svd_wide: core wider than 512");
+}
+
+int jacobi_staged_max_n() {
+  static int nmax = [] {
+    size_t lim = enable_max_dyn_smem(jacobi_svd_kernel);
+    int n = 1;
+    while ((size_t)2 * (n + 1) * (n + 1) * 8 <= lim) ++n;
+    return n;
+  }();
+  return nmax;
+}
+
 // ------------------------------------------------- SYMMETRIC JACOBI ------
 // Two-sided cyclic Jacobi for a small symmetric matrix B (n x n, n <= 160):
 // B = V diag(lam) V^T.  Each parallel step applies n/2 disjoint rotations
