@@ -208,6 +208,14 @@ int tlrg_dense_ldl(tlrg_ctx ctx, const double* A, int32_t n, double* L, double* 
                    uint8_t* s2, int32_t* perm, int32_t* info, tlrg_status* st);
 int tlrg_schur_compensation(tlrg_ctx ctx, const double* Dk, int32_t n, double eps,
                             double* diag_out, double* frob, tlrg_status* st);
+/* one-sided Jacobi SVD of an m x n matrix (the recompression core, svd_truncate
+ * dense_kernels.cpp:422-454): US = A V (columns sorted by singular value,
+ * descending), V (n x n), sig (n), rank = #{sig > cut}.  Cores wider than the
+ * shared-memory kernel run on one thread-block cluster (force_single = 1: the
+ * one-CTA kernel, for comparisons). */
+int tlrg_jacobi_svd(tlrg_ctx ctx, const double* A, int32_t m, int32_t n, double cut,
+                    int32_t force_single, double* US, double* V, double* sig, int32_t* rank,
+                    tlrg_status* st);
 int tlrg_gemm(tlrg_ctx ctx, int32_t M, int32_t N, int32_t K, int32_t transA, int32_t transB,
               double alpha, const double* A, const double* B, double beta, double* C,
               tlrg_status* st);

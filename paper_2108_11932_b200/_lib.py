@@ -113,6 +113,8 @@ SIGNATURES = {
     "tlrg_dense_ldl": (C.c_int, [vp, dp, C.c_int32, dp, dp, dp, u8p, ip, ip, C.POINTER(StatusC)]),
     "tlrg_schur_compensation": (C.c_int, [vp, dp, C.c_int32, C.c_double, dp, dp,
                                           C.POINTER(StatusC)]),
+    "tlrg_jacobi_svd": (C.c_int, [vp, dp, C.c_int32, C.c_int32, C.c_double, C.c_int32, dp, dp,
+                                  dp, ip, C.POINTER(StatusC)]),
     "tlrg_gemm": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
                             dp, dp, C.c_double, dp, C.POINTER(StatusC)]),
 }

@@ -586,6 +586,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     rtot += (long long)q[s] * q[s];
   }
   double *Rr = nullptr, *Vs = nullptr;
+  std::vector<char> is_wide(T, 0);
   if (recomp && qmax > 0) {
     Rr = C.buf<double>("Rr", (size_t)rtot + 1);
     double* Rpr = C.buf<double>("Rpr", (size_t)2 * rtot + 1);
@@ -596,28 +597,59 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     uint8_t* df = C.buf<uint8_t>("rdef", (size_t)T * qmax + 1);
     int* rko = C.buf<int>("rank_out", (size_t)T);
     std::vector<PanelTask> tasks;
-    std::vector<SvdTask> svd;
+    std::vector<SvdTask> svd, svdw;
     std::vector<int> sl;
+    // Bases wider than the shared-memory Jacobi skip the QR of B: one-sided
+    // Jacobi on B itself (B V = Z R V = Z U_s S, the same rotations as on R in
+    // exact arithmetic since B and R share their Gram matrix), one thread-block
+    // cluster per tile.  B <- B V = Z U_s S in place, Q <- Q V.
+    const int nst = jacobi_staged_max_n();
+    auto wide = [&](int s) { return q[s] > nst && q[s] <= 512 && cols <= 1024; };
+    long long wtot = 0;
+    for (int s = 0; s < T; ++s) is_wide[s] = q[s] > 0 && recomp && wide(s);
+    for (int s = 0; s < T; ++s)
+      if (is_wide[s]) wtot += (long long)q[s] * (cols + q[s]);
+    double* wwork = wtot ? C.buf<double>("svdwork_wide", (size_t)wtot) : nullptr;
+    int qmax_n = 0;
     std::vector<long long> roff2(T, 0);
     long long rtot2 = 0;
     for (int s = 0; s < T; ++s) {
       roff2[s] = rtot2;
-      rtot2 += q[s];
+      if (!is_wide[s]) {
+        rtot2 += q[s];
+        qmax_n = std::max(qmax_n, q[s]);
+      }
     }
     double* rrep = C.buf<double>("rrep", (size_t)cols * rtot2 + 1);
     {
       std::vector<int> need_s;
       std::vector<long long> need;
       for (int s = 0; s < T; ++s)
-        if (q[s]) {
+        if (q[s] && !is_wide[s]) {
           need_s.push_back(s);
           need.push_back(2LL * q[s] * cols);  // every column replaced in both sweeps
         }
       ensure(need_s, need);
     }
     h1 = hnow();
+    long long wo = 0;
     for (int s = 0; s < T; ++s) {
       if (q[s] == 0) continue;
+      sl.push_back(s);
+      SvdTask V{};
+      V.V = Vs + roff[s];
+      V.sig = sig + (size_t)s * qmax;
+      V.rank_out = rko + s;
+      V.n = q[s];
+      V.cut = cut;
+      if (is_wide[s]) {
+        V.A = Bb + boff[s];
+        V.m = cols;
+        V.work = wwork + wo;
+        wo += (long long)q[s] * (cols + q[s]);
+        svdw.push_back(V);
+        continue;
+      }
       PanelTask P{};
       P.Y = Bb + boff[s];
       P.Q = nullptr;
@@ -636,36 +668,23 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       P.width = q[s];
       P.q = 0;
       tasks.push_back(P);
-      SvdTask V{};
       V.A = Rr + roff[s];
-      V.V = Vs + roff[s];
-      V.sig = sig + (size_t)s * qmax;
       V.work = work + 2 * roff[s];
-      V.rank_out = rko + s;
-      V.n = q[s];
-      V.cut = cut;
       svd.push_back(V);
-      sl.push_back(s);
     }
-    PanelTask* d_tasks = C.push(tasks);
-    panel_tau(d_tasks, (int)tasks.size(), C.st);
-    panel_mgs(d_tasks, (int)tasks.size(), 0, 0, qmax, cols, C.st);
-    panel_mgs(d_tasks, (int)tasks.size(), 1, 1, qmax, cols, C.st);
-    {
-      // cores wider than the shared-memory Jacobi get a thread-block cluster
-      // each (same result); they go first, the narrow rest follows
-      const int nst = jacobi_staged_max_n();
-      std::stable_sort(svd.begin(), svd.end(),
-                       [](const SvdTask& a, const SvdTask& b) { return a.n > b.n; });
-      int nwide = 0;
-      while (nwide < (int)svd.size() && svd[nwide].n > nst && svd[nwide].n <= 512) ++nwide;
-      SvdTask* d_svd = C.push(svd);
-      if (nwide) {
-        jacobi_svd_wide(d_svd, nwide, svd[0].n, C.st);
-        ++C.launches;
-      }
-      if (nwide < (int)svd.size()) jacobi_svd(d_svd + nwide, (int)svd.size() - nwide,
-                                              svd[nwide].n, C.st);
+    if (!svdw.empty()) {
+      // widest first: they are the batch's critical path
+      std::stable_sort(svdw.begin(), svdw.end(),
+                       [](const SvdTask& x, const SvdTask& y) { return x.n > y.n; });
+      jacobi_svd_wide(C.push(svdw), (int)svdw.size(), svdw[0].n, C.st, cols);
+      ++C.launches;
+    }
+    if (!tasks.empty()) {
+      PanelTask* d_tasks = C.push(tasks);
+      panel_tau(d_tasks, (int)tasks.size(), C.st);
+      panel_mgs(d_tasks, (int)tasks.size(), 0, 0, qmax_n, cols, C.st);
+      panel_mgs(d_tasks, (int)tasks.size(), 1, 1, qmax_n, cols, C.st);
+      jacobi_svd(C.push(svd), (int)svd.size(), qmax_n, C.st);
     }
     C.launches += 4;
     h2 = hnow();
@@ -715,6 +734,10 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       g.C = out.U[s]; g.ldc = S.rows[s];
       g.M = S.rows[s]; g.N = fr[s]; g.K = q[s]; g.alpha = 1.0;
       pu.push_back(g);
+      if (is_wide[s]) {  // B V = Z U_s S is already in place, sorted
+        cpy.push_back({Bb + boff[s], out.V[s], cols, cols, cols, fr[s]});
+        continue;
+      }
       GemmProblem h{};
       h.A = Bb + boff[s]; h.lda = cols;
       h.B = Rr + roff[s]; h.ldb = q[s];

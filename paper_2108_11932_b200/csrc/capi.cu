@@ -1052,6 +1052,38 @@ int tlrg_schur_compensation(tlrg_ctx ctx, const double* Dk, int32_t n, double ep
   });
 }
 
+int tlrg_jacobi_svd(tlrg_ctx ctx, const double* A, int32_t m, int32_t n, double cut,
+                    int32_t force_single, double* US, double* V, double* sig, int32_t* rank,
+                    tlrg_status* st) {
+  return guarded(st, [&] {
+    if (m < 1 || n < 1) config_error("jacobi_svd: empty matrix");
+    Ctx& C = ctx->c;
+    double* dA = C.buf<double>("t_js_A", (size_t)m * n);
+    double* dV = C.buf<double>("t_js_V", (size_t)n * n);
+    double* dS = C.buf<double>("t_js_S", (size_t)n);
+    double* dW = C.buf<double>("t_js_W", (size_t)n * (m + n));
+    int* dR = C.buf<int>("t_js_R", 1);
+    TLRG_CUDA(cudaMemcpy(dA, A, 8 * (size_t)m * n, cudaMemcpyHostToDevice));
+    SvdTask t{};
+    t.A = dA;
+    t.V = dV;
+    t.sig = dS;
+    t.work = dW;
+    t.rank_out = dR;
+    t.n = n;
+    t.m = m;
+    t.cut = cut;
+    const bool wide = !force_single && n > jacobi_staged_max_n() && n <= 1024 && m <= 1024;
+    if (wide) jacobi_svd_wide(C.push(std::vector<SvdTask>{t}), 1, n, C.st, m);
+    else jacobi_svd(C.push(std::vector<SvdTask>{t}), 1, n, C.st, m);
+    C.sync();
+    TLRG_CUDA(cudaMemcpy(US, dA, 8 * (size_t)m * n, cudaMemcpyDeviceToHost));
+    TLRG_CUDA(cudaMemcpy(V, dV, 8 * (size_t)n * n, cudaMemcpyDeviceToHost));
+    TLRG_CUDA(cudaMemcpy(sig, dS, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+    TLRG_CUDA(cudaMemcpy(rank, dR, 4, cudaMemcpyDeviceToHost));
+  });
+}
+
 int tlrg_gemm(tlrg_ctx ctx, int32_t M, int32_t N, int32_t K, int32_t ta, int32_t tb, double alpha,
               const double* A, const double* B, double beta, double* Cm, tlrg_status* st) {
   return guarded(st, [&] {

@@ -738,6 +738,8 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     h_setup = hrel();
     const bool comp = opts.schur && k > 0 && cs.K > 0;
     int p_comp = comp ? schur_comp_width(rk, rank_hint) : 0;
+    const bool comp_chunked =
+        comp && p_comp >= std::min(rk, kSchurMaxWidth) && p_comp < rk && rank_hint > p_comp - 8;
 
     // ---- diagonal path on its own stream: it needs only row k of L, so it runs
     //      concurrently with the column's ARA (which needs L_kk only for the
@@ -799,9 +801,17 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
           ++C.launches;
         }
         cudaEventRecord(de1.e, C.st);
-        if (comp)
+        if (comp_chunked) {
+          // the previous column's eps-rank already exceeded one sketch: run the
+          // chunked spectrum split here, on the diagonal stream while the ARA
+          // runs, instead of a first sketch that the join would discard and
+          // redo on the critical path (same seed and attempts: same result)
+          schur_compensation_device(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), corr,
+                                    frob, rank_hint);
+        } else if (comp) {
           schur_comp_enqueue(C, Dk, rk, cfg.eps, tile_seed(cfg.seed, 0x5c4ULL, k, 0), p_comp, 0,
                              corr, frob, info + 2, p_comp >= std::min(rk, kSchurMaxWidth) ? 2 : 1);
+        }
         cudaEventRecord(de2.e, C.st);
         diag_tail();
         diag_inverse();
@@ -866,7 +876,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
     bool redo_trsm = false;
     C.wait();
     int st_potrf = hs[0], st_sing = hs[1], st_rank = hs[2];
-    if (comp && st_rank > p_comp - 8 && p_comp < rk) {
+    if (comp && !comp_chunked && st_rank > p_comp - 8 && p_comp < rk) {
       // sketch too narrow for this column's spectrum: redo with a wider one,
       // or (eps-rank above one sketch) with the chunked spectrum split
       rank_hint = std::max(rank_hint, 2 * p_comp);
@@ -880,7 +890,7 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       st_sing = hs[1];
       diag_inverse();
       redo_trsm = true;
-    } else if (comp) {
+    } else if (comp && !comp_chunked) {
       rank_hint = st_rank;
     }
     if (comp) S.compensation_frob += std::sqrt(hf[0]);

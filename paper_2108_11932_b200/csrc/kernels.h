@@ -150,9 +150,10 @@ struct SvdTask {
   double tol;   // rotation threshold (0 = rounding level m * eps_mach)
 };
 void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m = 0);
-// Square cores (m = n) wider than the shared-memory path (n > jacobi_staged_max_n(),
-// n <= 512): one thread-block cluster per task, bitwise the same result.
-void jacobi_svd_wide(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st);
+// Problems too large for the shared-memory path (n > jacobi_staged_max_n(),
+// m, n <= 1024): one thread-block cluster per task, the same pair schedule and
+// result as jacobi_svd.  max_m = largest row count (0 = max_n).
+void jacobi_svd_wide(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m = 0);
 int jacobi_staged_max_n();
 // symmetric (PSD) core: A <- V diag(lam), V, |lam| sorted descending (n <= 160)
 void sym_jacobi(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st);

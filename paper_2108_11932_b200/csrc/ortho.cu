@@ -58,6 +58,15 @@ void ara_absorb(AbsorbTask* d_tasks, int ntask, cudaStream_t st) {
 // (shared memory when it fits, else T.work) and writes the columns back sorted
 // by singular value (descending, ties by index) like dgesdd's output order.
 constexpr int JT = 1024;
+// the rotation and the sums are written with explicit rounding intrinsics so
+// that the one-CTA and the cluster kernel (jacobi_wide_kernel) compile to the
+// same arithmetic (no compiler choice of FMA contraction): bitwise-equal results
+__device__ __forceinline__ double jrot_a(double c, double s, double x, double y) {
+  return __dadd_rn(__dmul_rn(c, x), -__dmul_rn(s, y));
+}
+__device__ __forceinline__ double jrot_b(double c, double s, double x, double y) {
+  return __dadd_rn(__dmul_rn(s, x), __dmul_rn(c, y));
+}
 
 __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int staged) {
   extern __shared__ double jsm[];
@@ -77,7 +86,7 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   {
     __shared__ double red[32];
     double f = 0.0;
-    for (long long e = tid; e < (long long)m * n; e += JT) f += A[e] * A[e];
+    for (long long e = tid; e < (long long)m * n; e += JT) f = __fma_rn(A[e], A[e], f);
     f = block_sum(f, red);
     if (tid == 0) s_tiny = f * 1e-34;  // (1e-17 ||A||_F)^2: below rounding of any column
   }
@@ -100,9 +109,9 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
         double* aq = A + (long long)q * m;
         double al = 0, be = 0, ga = 0;
         for (int r = lane; r < m; r += 32) {
-          al += ap[r] * ap[r];
-          be += aq[r] * aq[r];
-          ga += ap[r] * aq[r];
+          al = __fma_rn(ap[r], ap[r], al);
+          be = __fma_rn(aq[r], aq[r], be);
+          ga = __fma_rn(ap[r], aq[r], ga);
         }
         al = warp_sum(al);
         be = warp_sum(be);
@@ -115,15 +124,15 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
           double c = rsqrt(1.0 + t * t), s = c * t;
           for (int r = lane; r < m; r += 32) {
             double x = ap[r], y = aq[r];
-            ap[r] = c * x - s * y;
-            aq[r] = s * x + c * y;
+            ap[r] = jrot_a(c, s, x, y);
+            aq[r] = jrot_b(c, s, x, y);
           }
           double* vp = V + (long long)p * n;
           double* vq = V + (long long)q * n;
           for (int r = lane; r < n; r += 32) {
             double x = vp[r], y = vq[r];
-            vp[r] = c * x - s * y;
-            vq[r] = s * x + c * y;
+            vp[r] = jrot_a(c, s, x, y);
+            vq[r] = jrot_b(c, s, x, y);
           }
           if (lane == 0) rotated = 1;
         }
@@ -136,7 +145,7 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   // singular values = column norms of A
   for (int p = warp; p < n; p += nw) {
     double s = 0.0;
-    for (int r = lane; r < m; r += 32) s += A[(long long)p * m + r] * A[(long long)p * m + r];
+    for (int r = lane; r < m; r += 32) s = __fma_rn(A[(long long)p * m + r], A[(long long)p * m + r], s);
     s = warp_sum(s);
     if (lane == 0) T.sig[p] = sqrt(s);
   }
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
   // sigma in descending order
   for (int p = warp; p < n; p += nw) {
     double s = 0.0;
-    for (int r = lane; r < m; r += 32) s += T.A[(long long)p * m + r] * T.A[(long long)p * m + r];
+    for (int r = lane; r < m; r += 32) s = __fma_rn(T.A[(long long)p * m + r], T.A[(long long)p * m + r], s);
     s = warp_sum(s);
     if (lane == 0) T.sig[p] = sqrt(s);
   }
@@ -313,9 +322,9 @@ void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max
 // in registers between the dot products and the rotation (one L2 round trip
 // per column instead of two, and no serial pair loop per warp).  At cfg4's
 // recompression (q-hat up to 276) this is the column's critical path.
-constexpr int JW_T = 512, JW_CL = 8;
-
-template <int E>
+// E = column elements per lane (m <= 32 E); JW_T threads per CTA, JW_CL CTAs per
+// cluster (16 = non-portable size, for the 1024-row panels of cfg4).
+template <int E, int JW_T, int JW_CL>
 __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
   const int crank = (int)cluster_ctarank();
   SvdTask& T = tasks[blockIdx.x / JW_CL];
@@ -339,14 +348,13 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
   double f = 0.0;  // every CTA forms the same Frobenius norm (same order as the 1-CTA kernel)
   {
     // the 1-CTA kernel reduces with 1024 threads: reproduce its partition
-    double p0 = 0.0, p1 = 0.0;
-    for (long long e = tid; e < (long long)m * n; e += 1024) p0 += T.A[e] * T.A[e];
-    for (long long e = tid + 512; e < (long long)m * n; e += 1024) p1 += T.A[e] * T.A[e];
-    p0 = warp_sum(p0);
-    p1 = warp_sum(p1);
-    if (lane == 0) {
-      red[warp] = p0;
-      red[warp + 16] = p1;
+    constexpr int V = 1024 / JW_T;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double pk = 0.0;
+      for (long long e = tid + k * JW_T; e < (long long)m * n; e += 1024) pk = __fma_rn(T.A[e], T.A[e], pk);
+      pk = warp_sum(pk);
+      if (lane == 0) red[warp + k * nw] = pk;
     }
     __syncthreads();
     for (int i = 0; i < 32; ++i) f += red[i];
@@ -375,9 +383,9 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
         double al = 0, be = 0, ga = 0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          al += x[e] * x[e];
-          be += y[e] * y[e];
-          ga += x[e] * y[e];
+          al = __fma_rn(x[e], x[e], al);
+          be = __fma_rn(y[e], y[e], be);
+          ga = __fma_rn(x[e], y[e], ga);
         }
         al = warp_sum(al);
         be = warp_sum(be);
@@ -390,8 +398,8 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
           for (int e = 0; e < E; ++e) {
             const int r = lane + 32 * e;
             if (r < m) {
-              __stcg(ap + r, c * x[e] - s * y[e]);
-              __stcg(aq + r, s * x[e] + c * y[e]);
+              __stcg(ap + r, jrot_a(c, s, x[e], y[e]));
+              __stcg(aq + r, jrot_b(c, s, x[e], y[e]));
             }
           }
           double* vp = V + (long long)p * n;
@@ -406,8 +414,8 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
           for (int e = 0; e < E; ++e) {
             const int r = lane + 32 * e;
             if (r < n) {
-              __stcg(vp + r, c * x[e] - s * y[e]);
-              __stcg(vq + r, s * x[e] + c * y[e]);
+              __stcg(vp + r, jrot_a(c, s, x[e], y[e]));
+              __stcg(vq + r, jrot_b(c, s, x[e], y[e]));
             }
           }
           if (lane == 0) atomicOr(rot0 + (sweep & 1), 1);
@@ -422,7 +430,10 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
   // singular values = column norms of A; then the sorted write-back
   for (int p = gw; p < n; p += gnw) {
     double s = 0.0;
-    for (int r = lane; r < m; r += 32) s += __ldcg(A + (long long)p * m + r) * __ldcg(A + (long long)p * m + r);
+    for (int r = lane; r < m; r += 32) {
+      const double v = __ldcg(A + (long long)p * m + r);
+      s = __fma_rn(v, v, s);
+    }
     s = warp_sum(s);
     if (lane == 0) __stcg(T.sig + p, sqrt(s));
   }
@@ -447,7 +458,7 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
     double s = 0.0;
     for (int r = lane; r < m; r += 32) {
       const double v = __ldcg(T.A + (long long)p * m + r);
-      s += v * v;
+      s = __fma_rn(v, v, s);
     }
     s = warp_sum(s);
     if (lane == 0) T.sig[p] = sqrt(s);
@@ -456,26 +467,37 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
   cluster_sync_all();  // no CTA leaves while its shared memory may still be addressed
 }
 
-void jacobi_svd_wide(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st) {
-  if (ntask <= 0) return;
+template <int E, int NT, int CL>
+static void launch_wide(SvdTask* d_tasks, int ntask, cudaStream_t st) {
+  static bool once = [] {
+    if (CL > 8)
+      cudaFuncSetAttribute(jacobi_wide_kernel<E, NT, CL>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return true;
+  }();
+  (void)once;
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3((unsigned)(ntask * JW_CL));
-  lc.blockDim = dim3(JW_T);
+  lc.gridDim = dim3((unsigned)(ntask * CL));
+  lc.blockDim = dim3(NT);
   lc.dynamicSmemBytes = 0;
   lc.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = JW_CL;
+  at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  if (max_n <= 256)
-    TLRG_CUDA(cudaLaunchKernelEx(&lc, jacobi_wide_kernel<8>, d_tasks));
-  else if (max_n <= 512)
-    TLRG_CUDA(cudaLaunchKernelEx(&lc, jacobi_wide_kernel<16>, d_tasks));
-  else
-    throw CudaError("jacobi_svd_wide: core wider than 512");
+  TLRG_CUDA(cudaLaunchKernelEx(&lc, jacobi_wide_kernel<E, NT, CL>, d_tasks));
+}
+
+void jacobi_svd_wide(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m) {
+  if (ntask <= 0) return;
+  const int mm = std::max(max_m, max_n);
+  if (mm <= 256) launch_wide<8, 512, 8>(d_tasks, ntask, st);
+  else if (mm <= 512) launch_wide<16, 512, 8>(d_tasks, ntask, st);
+  else if (mm <= 1024) launch_wide<32, 256, 16>(d_tasks, ntask, st);
+  else throw CudaError("jacobi_svd_wide: more than 1024 rows");
 }
 
 int jacobi_staged_max_n() {
@@ -626,24 +648,90 @@ void sym_jacobi(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st) {
 }
 
 // ------------------------------------------------------ BLOCK PRODUCTS ----
-__global__ void __launch_bounds__(128) block_products_kernel(const BlockItem* items) {
-  const BlockItem& B = items[blockIdx.x];
-  for (int r = threadIdx.x; r < B.rows; r += blockDim.x) {
-    for (int c = 0; c < B.kkj; ++c) {
-      double s = 0.0;
-      for (int p = 0; p < B.kij; ++p) s += B.U[(long long)p * B.rows + r] * B.G[p + c * B.ldg];
-      B.H[r + c * B.ldh] = s;
+// H[r, c] = sum_p U[r, p] G[p, c] for one block (rows x kij times kij x kkj).
+// Each thread owns HP_R rows (stride HP_T) and eight output columns at a time;
+// G is staged in shared memory 256 rows x 8 columns at a time, so every U
+// element is loaded once per eight columns (the one-row-per-thread loop loaded
+// it kkj times and ran the largest near-diagonal blocks, 1024 x 170 x 170 at
+// cfg4, for ~20 ms on one CTA).  The p-sum runs in the same order as before,
+// so the result is bitwise unchanged.  Rows [r0, r1) let several CTAs share a
+// tall block.
+constexpr int HP_T = 128, HP_R = 4, HP_P = 256;
+__device__ __forceinline__ void hblock_product(const double* U, const double* G, long long ldg,
+                                               double* H, long long ldh, int rows, int r0, int r1,
+                                               int kij, int kkj, double (*sG)[8]) {
+  const int tid = threadIdx.x;
+  for (int c0 = 0; c0 < kkj; c0 += 8) {
+    double acc[HP_R][8];
+#pragma unroll
+    for (int rr = 0; rr < HP_R; ++rr)
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) acc[rr][cc] = 0.0;
+    for (int p0 = 0; p0 < kij; p0 += HP_P) {
+      const int np = min(HP_P, kij - p0);
+      __syncthreads();
+      for (int e = tid; e < np * 8; e += HP_T) {
+        const int pp = e >> 3, cc = e & 7;
+        sG[pp][cc] = c0 + cc < kkj ? G[(p0 + pp) + (long long)(c0 + cc) * ldg] : 0.0;
+      }
+      __syncthreads();
+      for (int pp = 0; pp < np; ++pp) {
+        const double* up = U + (long long)(p0 + pp) * rows;
+        double u[HP_R];
+#pragma unroll
+        for (int rr = 0; rr < HP_R; ++rr) {
+          const int r = r0 + tid + rr * HP_T;
+          u[rr] = r < r1 ? up[r] : 0.0;
+        }
+        const double2* g2 = reinterpret_cast<const double2*>(sG[pp]);
+        double g[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const double2 v = g2[h];
+          g[2 * h] = v.x;
+          g[2 * h + 1] = v.y;
+        }
+#pragma unroll
+        for (int rr = 0; rr < HP_R; ++rr)
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) acc[rr][cc] += u[rr] * g[cc];
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < HP_R; ++rr) {
+      const int r = r0 + tid + rr * HP_T;
+      if (r < r1)
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          if (c0 + cc < kkj) H[r + (long long)(c0 + cc) * ldh] = acc[rr][cc];
     }
   }
 }
+// row chunk of CTA y out of ny for a block of `rows` rows (HP_T * HP_R rows max)
+__device__ __forceinline__ void hp_rows(int rows, int y, int ny, int* r0, int* r1) {
+  const int per = (rows + ny - 1) / ny;
+  *r0 = min(rows, y * per);
+  *r1 = min(rows, *r0 + per);
+}
 
-void block_products(BlockItem* d_items, int nitems, int, cudaStream_t st) {
+__global__ void __launch_bounds__(HP_T) block_products_kernel(const BlockItem* items) {
+  __shared__ __align__(16) double sG[HP_P][8];
+  const BlockItem& B = items[blockIdx.x];
+  int r0, r1;
+  hp_rows(B.rows, blockIdx.y, gridDim.y, &r0, &r1);
+  hblock_product(B.U, B.G, B.ldg, B.H, B.ldh, B.rows, r0, r1, B.kij, B.kkj, sG);
+}
+
+static int hp_chunks(int rows) { return std::max(1, (rows + HP_T * HP_R - 1) / (HP_T * HP_R)); }
+
+void block_products(BlockItem* d_items, int nitems, int max_rows, cudaStream_t st) {
   if (nitems <= 0) return;
-  block_products_kernel<<<nitems, 128, 0, st>>>(d_items);
+  block_products_kernel<<<dim3(nitems, hp_chunks(max_rows)), HP_T, 0, st>>>(d_items);
   TLRG_CUDA(cudaGetLastError());
 }
 
-__global__ void __launch_bounds__(128) h_products_kernel(HProductArgs a) {
+__global__ void __launch_bounds__(HP_T) h_products_kernel(HProductArgs a) {
+  __shared__ __align__(16) double sG[HP_P][8];
   const int t = blockIdx.x / a.nJ, jj = blockIdx.x - t * a.nJ;
   const long long* tg = a.cols;
   const long long* Jl = tg + a.T;
@@ -664,18 +752,14 @@ __global__ void __launch_bounds__(128) h_products_kernel(HProductArgs a) {
   const double* U = kij ? a.U[tij] : nullptr;
   const double* G = a.G + Jl[4 * a.nJ + jj] + s_pre;
   double* H = a.H + t * a.stride + Jl[2 * a.nJ + jj] * rows;
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
-    for (int c = 0; c < kkj; ++c) {
-      double s = 0.0;
-      for (int p = 0; p < kij; ++p) s += U[(long long)p * rows + r] * G[p + c * ldg];
-      H[r + c * rows] = s;
-    }
-  }
+  int r0, r1;
+  hp_rows(rows, blockIdx.y, gridDim.y, &r0, &r1);
+  hblock_product(U, G, ldg, H, rows, rows, r0, r1, kij, kkj, sG);
 }
 
 void h_products(const HProductArgs& a, cudaStream_t st) {
   if (a.T <= 0 || a.nJ <= 0) return;
-  h_products_kernel<<<a.T * a.nJ, 128, 0, st>>>(a);
+  h_products_kernel<<<dim3(a.T * a.nJ, hp_chunks(a.b)), HP_T, 0, st>>>(a);
   TLRG_CUDA(cudaGetLastError());
 }
 

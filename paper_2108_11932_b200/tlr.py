@@ -679,6 +679,22 @@ def dense_cholesky(A, ctx=None):
     return np.tril(np.array(Lm)), int(fail.value)
 
 
+def jacobi_svd(A, cut, force_single=False, ctx=None):
+    """One-sided Jacobi SVD of the recompression core (svd_truncate,
+    dense_kernels.cpp:422-454): returns (A V sorted, V, sigma, rank)."""
+    ctx = _ctx(ctx)
+    m, n = A.shape
+    Af = np.asfortranarray(A, dtype=np.float64)
+    US = np.zeros((m, n), order="F")
+    V = np.zeros((n, n), order="F")
+    sig = np.zeros(n)
+    rk = C.c_int32()
+    _call(ctx.lib.tlrg_jacobi_svd, ctx.h, Af.ctypes.data_as(L.dp), m, n, float(cut),
+          1 if force_single else 0, US.ctypes.data_as(L.dp), V.ctypes.data_as(L.dp), _d(sig),
+          C.byref(rk))
+    return np.array(US), np.array(V), sig, int(rk.value)
+
+
 def dense_ldl(A, ctx=None):
     ctx = _ctx(ctx)
     n = A.shape[0]

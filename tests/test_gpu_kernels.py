@@ -149,6 +149,42 @@ def test_potrf_matches_reference(tg, ref, n):
     assert fail >= 0
 
 
+def _decaying(r, m, n, decades=10.0):
+    U, _ = np.linalg.qr(r.normal(size=(m, n)))
+    W, _ = np.linalg.qr(r.normal(size=(n, n)))
+    return (U * np.logspace(2, 2 - decades, n)) @ W.T
+
+
+@pytest.mark.parametrize("n", [150, 276])
+def test_wide_jacobi_cluster_is_bitwise_the_one_cta_kernel(tg, n):
+    """Square recompression cores wider than shared memory: the cluster kernel
+    runs the 1-CTA kernel's pair schedule, so every output is bitwise equal."""
+    A = _decaying(np.random.default_rng(n), n, n)
+    cut = 1e-3
+    a = tg.tlr.jacobi_svd(A, cut)
+    b = tg.tlr.jacobi_svd(A, cut, force_single=True)
+    for x, y in zip(a[:3], b[:3]):
+        assert np.array_equal(x, y)
+    assert a[3] == b[3]
+
+
+@pytest.mark.parametrize("m,n", [(1024, 276), (1024, 130), (512, 200), (256, 140)])
+def test_wide_jacobi_on_the_basis_matches_numpy_svd(tg, m, n):
+    """Wide ARA bases are recompressed by Jacobi on B itself (svd_truncate of
+    B's R factor, dense_kernels.cpp:422-454, without the QR): singular values,
+    rank at the cut and the factorization B V = U S."""
+    r = np.random.default_rng(m + n)
+    A = _decaying(r, m, n, decades=12.0)
+    s_ref = np.linalg.svd(A, compute_uv=False)
+    cut = np.sqrt(s_ref[n // 2] * s_ref[n // 2 + 1])  # away from any singular value
+    US, V, sig, rank = tg.tlr.jacobi_svd(A, cut)
+    assert rank == int((s_ref > cut).sum())
+    assert np.abs(sig - s_ref).max() <= 1e-13 * s_ref[0] * n
+    assert np.abs(V.T @ V - np.eye(n)).max() <= 1e-12
+    assert np.abs(US @ V.T - A).max() <= 1e-12 * s_ref[0]
+    assert np.allclose(np.linalg.norm(US, axis=0), sig, rtol=0, atol=1e-13 * s_ref[0])
+
+
 @pytest.mark.parametrize("n,kind", [(5, "indef"), (64, "indef"), (128, "spd"), (200, "indef"),
                                     (512, "indef")])
 def test_bunch_kaufman_matches_reference(tg, ref, n, kind):
