@@ -424,8 +424,19 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
   PanelTask* d_tasks = C.push(tasks);
   // ---- the round loop: one CUDA graph, conditional WHILE node on device ------
   tm.start(C.st);
+  // the gaussian rings are refilled on a side branch of the round (fork after
+  // this round's Omega is copied out, join before the loop condition): the
+  // sequential mt19937_64 + polar generation overlaps the products and sweeps
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  TLRG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  TLRG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  const long long topup_low = G.cap - 2LL * cols * bs;
   auto enqueue_round = [&]() {
     gauss_round(G, done, d_rows, T, cols, bs, Om, C.st);
+    TLRG_CUDA(cudaEventRecord(ev_fork, C.st));
+    TLRG_CUDA(cudaStreamWaitEvent(C.st2, ev_fork, 0));
+    gauss_topup(G, done, T, topup_low, C.st2);
+    TLRG_CUDA(cudaEventRecord(ev_join, C.st2));
     for (auto& pl : sample_plans) gemm_launch(pl, C.st);
     panel_tau(d_tasks, T, C.st);
     for (int sweep = 0; sweep < 2; ++sweep) {
@@ -433,6 +444,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       gemm_launch(plan_y, C.st);  // Y -= Q C       (dense_kernels.cpp:400)
       panel_mgs(d_tasks, T, sweep, sweep == 1, bs, maxrows, C.st);
     }
+    TLRG_CUDA(cudaStreamWaitEvent(C.st, ev_join, 0));
   };
   const char* ng = std::getenv("TLRG_NO_GRAPH");
   if (ng && ng[0] == '1') {
@@ -468,6 +480,8 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     TLRG_CUDA(cudaGraphLaunch(exec, C.st));
     graph_cleanup.push_back({exec, graph});
   }
+  cudaEventDestroy(ev_fork);
+  cudaEventDestroy(ev_join);
   }
   tm.stop(C.st);
   if (on_launch) on_launch();
@@ -604,7 +618,13 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     // exact arithmetic since B and R share their Gram matrix), one thread-block
     // cluster per tile.  B <- B V = Z U_s S in place, Q <- Q V.
     const int nst = jacobi_staged_max_n();
-    auto wide = [&](int s) { return q[s] > nst && q[s] <= 512 && cols <= 1024; };
+    const char* wbe = std::getenv("TLRG_WIDE_B");  // 0: QR + Jacobi on R for every tile (A/B)
+    const bool wide_b = !(wbe && wbe[0] == '0');
+    // (tall panels only: for cols < 512 the QR of B is cheap and the R core
+    // goes to the cluster Jacobi below, bitwise the reference-shaped path)
+    auto wide = [&](int s) {
+      return wide_b && q[s] > nst && q[s] <= 512 && cols >= 512 && cols <= 1024;
+    };
     long long wtot = 0;
     for (int s = 0; s < T; ++s) is_wide[s] = q[s] > 0 && recomp && wide(s);
     for (int s = 0; s < T; ++s)
@@ -684,7 +704,18 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       panel_tau(d_tasks, (int)tasks.size(), C.st);
       panel_mgs(d_tasks, (int)tasks.size(), 0, 0, qmax_n, cols, C.st);
       panel_mgs(d_tasks, (int)tasks.size(), 1, 1, qmax_n, cols, C.st);
-      jacobi_svd(C.push(svd), (int)svd.size(), qmax_n, C.st);
+      // R cores wider than the shared-memory Jacobi: one cluster each, first
+      std::stable_sort(svd.begin(), svd.end(),
+                       [](const SvdTask& x, const SvdTask& y) { return x.n > y.n; });
+      int nwr = 0;
+      while (nwr < (int)svd.size() && svd[nwr].n > nst && svd[nwr].n <= 1024) ++nwr;
+      SvdTask* d_svd = C.push(svd);
+      if (nwr) {
+        jacobi_svd_wide(d_svd, nwr, svd[0].n, C.st);
+        ++C.launches;
+      }
+      if (nwr < (int)svd.size())
+        jacobi_svd(d_svd + nwr, (int)svd.size() - nwr, svd[nwr].n, C.st);
     }
     C.launches += 4;
     h2 = hnow();

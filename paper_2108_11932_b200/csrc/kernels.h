@@ -76,6 +76,10 @@ void gauss_gather(const GaussStreams& G, const int* d_slots, int n, double* out,
 // deficient-column replacement are available, then copy Omega_s to Om + s*cols*bs.
 void gauss_round(const GaussStreams& G, const int* done, const int* rows, int nslots, int cols,
                  int bs, double* Om, cudaStream_t st);
+// refill the rings of the not-done slots to capacity when fewer than `low`
+// values are ahead of the cursor (the round graph runs it on a side branch)
+void gauss_topup(const GaussStreams& G, const int* done, int nslots, long long low,
+                 cudaStream_t st);
 
 // --------------------------------------------------------------- ORTHOG ---
 // One panel of the reference's orthog (dense_kernels.cpp:331-420) per task.

@@ -158,6 +158,21 @@ __global__ void __launch_bounds__(RT) gauss_round_kernel(GaussStreams G, const i
   if (threadIdx.x == 0) G.cursor[s] = cur + n;
 }
 
+// Ring top-up off the round's critical path: generate the slot's stream until
+// the ring is full again (ring_target caps at cursor + cap, so only consumed
+// positions are overwritten).  Runs concurrently with the round's products and
+// panel sweeps, which only read the ring and advance the cursor: a cursor read
+// here that is already stale only under-estimates the free space.
+__global__ void __launch_bounds__(RT) gauss_topup_kernel(GaussStreams G, const int* done,
+                                                         long long low) {
+  __shared__ GenSmem S;
+  const int s = blockIdx.x;
+  if (done[s]) return;
+  const long long cur = *reinterpret_cast<volatile long long*>(G.cursor + s), av = G.avail[s];
+  if (av - cur >= low) return;
+  cta_generate(G, s, av, ring_target(G, cur, cur + G.cap), S);
+}
+
 __global__ void __launch_bounds__(256) gauss_gather_kernel(GaussStreams G, const int* slots,
                                                            double* out, long long count,
                                                            long long out_stride) {
@@ -186,6 +201,13 @@ void gauss_round(const GaussStreams& G, const int* done, const int* rows, int ns
                  int bs, double* Om, cudaStream_t st) {
   if (nslots <= 0) return;
   gauss_round_kernel<<<nslots, RT, 0, st>>>(G, done, rows, cols, bs, Om);
+  TLRG_CUDA(cudaGetLastError());
+}
+
+void gauss_topup(const GaussStreams& G, const int* done, int nslots, long long low,
+                 cudaStream_t st) {
+  if (nslots <= 0) return;
+  gauss_topup_kernel<<<nslots, RT, 0, st>>>(G, done, low);
   TLRG_CUDA(cudaGetLastError());
 }
 

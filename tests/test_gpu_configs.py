@@ -152,13 +152,16 @@ def test_factor_of_a_borrowed_L_view_copies_it(tg, ref):
 
 def test_ldlt_solve_error_over_seeds(tg, ref):
     """cfg3 family (LDL^T, bs = 32, m = 512): backward and forward solve error
-    within 2x of the reference as the geometric mean over four ARA seeds, on the
-    same reference-built A (the per-seed spread of either side is 10x)."""
+    within 2x of the reference as the geometric mean over sixteen ARA seeds, on
+    the same reference-built A.  Either side's per-seed errors are heavy-tailed
+    (Bunch-Kaufman pivot choices flip under O(1e-12) perturbations of the
+    panels; the reference alone spans 2.7e-5 .. 6.0e-3 backward error over
+    seeds 1-16), so four seeds did not pin the mean (tools/ldlt_seeds.py)."""
     n, b, eps, bs = 8192, 512, 1e-4, 32
     A_ref = ref.build(points(G.GRID3D, n, b, 0), 1, 0.2, 1e-4, b, eps, 0, bs, SEED)
     A = to_gpu(tg, A_ref)
     ours, theirs = [], []
-    for sd in (1, 2, 4, SEED):
+    for sd in range(1, 17):
         F_ref = ref.factor(A_ref, 1, bs=bs, eps=eps, seed=sd)
         ra = ref.accuracy(A_ref, F_ref)
         oa = tg.tlr.accuracy(A, tg.tlr_ldlt(A.copy(), tg.AraConfig(block_samples=bs, eps=eps,
