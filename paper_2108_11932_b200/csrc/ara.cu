@@ -692,6 +692,17 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       V.work = work + 2 * roff[s];
       svd.push_back(V);
     }
+    // the wide tiles' clusters occupy few SMs for the batch's longest time: the
+    // narrow tiles' QR + Jacobi run beside them on the side stream
+    cudaEvent_t rfork = nullptr, rjoin = nullptr;
+    const bool split = !svdw.empty() && !tasks.empty();
+    cudaStream_t st_main = C.st;
+    if (split) {
+      TLRG_CUDA(cudaEventCreateWithFlags(&rfork, cudaEventDisableTiming));
+      TLRG_CUDA(cudaEventCreateWithFlags(&rjoin, cudaEventDisableTiming));
+      TLRG_CUDA(cudaEventRecord(rfork, C.st));
+      TLRG_CUDA(cudaStreamWaitEvent(C.st2, rfork, 0));
+    }
     if (!svdw.empty()) {
       // widest first: they are the batch's critical path
       std::stable_sort(svdw.begin(), svdw.end(),
@@ -699,6 +710,7 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       jacobi_svd_wide(C.push(svdw), (int)svdw.size(), svdw[0].n, C.st, cols);
       ++C.launches;
     }
+    if (split) C.st = C.st2;
     if (!tasks.empty()) {
       PanelTask* d_tasks = C.push(tasks);
       panel_tau(d_tasks, (int)tasks.size(), C.st);
@@ -716,6 +728,13 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       }
       if (nwr < (int)svd.size())
         jacobi_svd(d_svd + nwr, (int)svd.size() - nwr, svd[nwr].n, C.st);
+    }
+    if (split) {
+      C.st = st_main;
+      TLRG_CUDA(cudaEventRecord(rjoin, C.st2));
+      TLRG_CUDA(cudaStreamWaitEvent(C.st, rjoin, 0));
+      cudaEventDestroy(rfork);
+      cudaEventDestroy(rjoin);
     }
     C.launches += 4;
     h2 = hnow();

@@ -322,9 +322,11 @@ void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max
 // in registers between the dot products and the rotation (one L2 round trip
 // per column instead of two, and no serial pair loop per warp).  At cfg4's
 // recompression (q-hat up to 276) this is the column's critical path.
-// E = column elements per lane (m <= 32 E); JW_T threads per CTA, JW_CL CTAs per
-// cluster (16 = non-portable size, for the 1024-row panels of cfg4).
-template <int E, int JW_T, int JW_CL>
+// E = column elements per lane (m <= 32 E); EV > 0: the two V columns (n <= 32 EV)
+// are loaded with the A columns (one L2 round trip per pair instead of two);
+// JW_T threads per CTA, JW_CL CTAs per cluster (16 = non-portable size, for the
+// 1024-row panels of cfg4).
+template <int E, int EV, int JW_T, int JW_CL>
 __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
   const int crank = (int)cluster_ctarank();
   SvdTask& T = tasks[blockIdx.x / JW_CL];
@@ -373,12 +375,21 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
         if (p >= n || q >= n) continue;
         double* ap = A + (long long)p * m;
         double* aq = A + (long long)q * m;
+        double* vp = V + (long long)p * n;
+        double* vq = V + (long long)q * n;
         double x[E], y[E];
+        double xv[EV > 0 ? EV : 1], yv[EV > 0 ? EV : 1];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const int r = lane + 32 * e;
           x[e] = r < m ? __ldcg(ap + r) : 0.0;
           y[e] = r < m ? __ldcg(aq + r) : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {
+          const int r = lane + 32 * e;
+          xv[e] = r < n ? __ldcg(vp + r) : 0.0;
+          yv[e] = r < n ? __ldcg(vq + r) : 0.0;
         }
         double al = 0, be = 0, ga = 0;
 #pragma unroll
@@ -402,20 +413,29 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
               __stcg(aq + r, jrot_b(c, s, x[e], y[e]));
             }
           }
-          double* vp = V + (long long)p * n;
-          double* vq = V + (long long)q * n;
+          if (EV > 0) {
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int r = lane + 32 * e;
-            x[e] = r < n ? __ldcg(vp + r) : 0.0;
-            y[e] = r < n ? __ldcg(vq + r) : 0.0;
-          }
+            for (int e = 0; e < (EV > 0 ? EV : 1); ++e) {
+              const int r = lane + 32 * e;
+              if (r < n) {
+                __stcg(vp + r, jrot_a(c, s, xv[e], yv[e]));
+                __stcg(vq + r, jrot_b(c, s, xv[e], yv[e]));
+              }
+            }
+          } else {
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int r = lane + 32 * e;
-            if (r < n) {
-              __stcg(vp + r, jrot_a(c, s, x[e], y[e]));
-              __stcg(vq + r, jrot_b(c, s, x[e], y[e]));
+            for (int e = 0; e < E; ++e) {
+              const int r = lane + 32 * e;
+              x[e] = r < n ? __ldcg(vp + r) : 0.0;
+              y[e] = r < n ? __ldcg(vq + r) : 0.0;
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int r = lane + 32 * e;
+              if (r < n) {
+                __stcg(vp + r, jrot_a(c, s, x[e], y[e]));
+                __stcg(vq + r, jrot_b(c, s, x[e], y[e]));
+              }
             }
           }
           if (lane == 0) atomicOr(rot0 + (sweep & 1), 1);
@@ -467,11 +487,11 @@ __global__ void __launch_bounds__(JW_T) jacobi_wide_kernel(SvdTask* tasks) {
   cluster_sync_all();  // no CTA leaves while its shared memory may still be addressed
 }
 
-template <int E, int NT, int CL>
+template <int E, int EV, int NT, int CL>
 static void launch_wide(SvdTask* d_tasks, int ntask, cudaStream_t st) {
   static bool once = [] {
     if (CL > 8)
-      cudaFuncSetAttribute(jacobi_wide_kernel<E, NT, CL>,
+      cudaFuncSetAttribute(jacobi_wide_kernel<E, EV, NT, CL>,
                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return true;
   }();
@@ -488,15 +508,16 @@ static void launch_wide(SvdTask* d_tasks, int ntask, cudaStream_t st) {
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  TLRG_CUDA(cudaLaunchKernelEx(&lc, jacobi_wide_kernel<E, NT, CL>, d_tasks));
+  TLRG_CUDA(cudaLaunchKernelEx(&lc, jacobi_wide_kernel<E, EV, NT, CL>, d_tasks));
 }
 
 void jacobi_svd_wide(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m) {
   if (ntask <= 0) return;
   const int mm = std::max(max_m, max_n);
-  if (mm <= 256) launch_wide<8, 512, 8>(d_tasks, ntask, st);
-  else if (mm <= 512) launch_wide<16, 512, 8>(d_tasks, ntask, st);
-  else if (mm <= 1024) launch_wide<32, 256, 16>(d_tasks, ntask, st);
+  if (mm <= 256) launch_wide<8, 8, 512, 8>(d_tasks, ntask, st);
+  else if (mm <= 512) launch_wide<16, 0, 512, 8>(d_tasks, ntask, st);
+  else if (mm <= 1024 && max_n <= 288) launch_wide<32, 9, 256, 16>(d_tasks, ntask, st);
+  else if (mm <= 1024) launch_wide<32, 0, 256, 16>(d_tasks, ntask, st);
   else throw CudaError("jacobi_svd_wide: more than 1024 rows");
 }
 
