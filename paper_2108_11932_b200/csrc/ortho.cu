@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(JT) jacobi_svd_kernel(SvdTask* tasks, int stag
 // memory, but instruction-lean: 256 threads, EIGHT lanes per column pair (4
 // pairs per warp, 3-level shuffle reductions), pair lists precomputed per
 // step.  The kernels on this path are issue-bound on a single SM.
-constexpr int JS_T = 256;
+// JS_T = 256 threads give 32 pair slots per pass; cores with more than 32 pairs
+// (n > 64) take the 512-thread instance so every step is one pass.
+template <int JS_T>
 __global__ void __launch_bounds__(JS_T) jacobi_small_kernel(SvdTask* tasks) {
   extern __shared__ double jsm2[];
   SvdTask& T = tasks[blockIdx.x];
@@ -298,12 +300,14 @@ __global__ void __launch_bounds__(JS_T) jacobi_small_kernel(SvdTask* tasks) {
 
 void jacobi_svd(SvdTask* d_tasks, int ntask, int max_n, cudaStream_t st, int max_m) {
   static size_t lim = enable_max_dyn_smem(jacobi_svd_kernel);
-  static size_t lim2 = enable_max_dyn_smem(jacobi_small_kernel);
+  static size_t lim2 = std::min(enable_max_dyn_smem(jacobi_small_kernel<256>),
+                                enable_max_dyn_smem(jacobi_small_kernel<512>));
   if (ntask <= 0) return;
   if (max_m <= 0) max_m = max_n;
   size_t bytes = ((size_t)max_m * max_n + (size_t)max_n * max_n) * 8;
   if (max_n <= 128 && bytes <= lim2) {
-    jacobi_small_kernel<<<ntask, JS_T, bytes, st>>>(d_tasks);
+    if (max_n > 64) jacobi_small_kernel<512><<<ntask, 512, bytes, st>>>(d_tasks);
+    else jacobi_small_kernel<256><<<ntask, 256, bytes, st>>>(d_tasks);
     TLRG_CUDA(cudaGetLastError());
     return;
   }

@@ -9,7 +9,13 @@ kind, n, b, eps, bs, kern, ell, nug, mode = bench.CONFIGS[cfgname]
 A = build_tlr(bench.problem_points(cfgname), kern, ell, nug, b, eps,
               cfg=tg.AraConfig(block_samples=bs, seed=12345))
 ctx = A.ctx
-ctx.lib.tlrg_profiler(1)
-F = (tg.tlr_cholesky if mode == 0 else tg.tlr_ldlt)(A, tg.AraConfig(block_samples=bs, eps=eps, seed=12345))
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # > 1: warm repeats (the last is profiled)
+for rep in range(reps):
+    if rep == reps - 1:
+        ctx.lib.tlrg_profiler(1)
+        print("=== profiled run", file=sys.stderr, flush=True)
+    Ain = A.copy() if rep < reps - 1 else A
+    F = (tg.tlr_cholesky if mode == 0 else tg.tlr_ldlt)(Ain, tg.AraConfig(block_samples=bs, eps=eps, seed=12345))
+    print("t_device", F.stats.t_device, "launches", F.stats.kernel_launches, flush=True)
+    del F
 ctx.lib.tlrg_profiler(0)
-print("t_device", F.stats.t_device, "launches", F.stats.kernel_launches)
