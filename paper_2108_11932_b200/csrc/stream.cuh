@@ -88,13 +88,29 @@ __device__ inline void cta_generate(GaussStreams& G, int s, long long have, long
   __syncthreads();
 }
 
+// dst[0..n) <- src[0..n) with eight loads in flight per thread (the plain
+// loop keeps one: without restrict the store may alias the next load)
+__device__ __forceinline__ void copy_span(const double* __restrict__ src,
+                                          double* __restrict__ dst, long long n, int nthreads) {
+  constexpr int U = 8;
+  long long e = threadIdx.x;
+  for (; e + (long long)(U - 1) * nthreads < n; e += (long long)U * nthreads) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = src[e + (long long)u * nthreads];
+#pragma unroll
+    for (int u = 0; u < U; ++u) dst[e + (long long)u * nthreads] = v[u];
+  }
+  for (; e < n; e += nthreads) dst[e] = src[e];
+}
+
 // dst[0..n) <- ring[(pos + e) mod cap], without a per-element modulo
 __device__ __forceinline__ void ring_copy(const double* ring, long long cap, long long pos,
                                           long long n, double* dst, int nthreads) {
   const long long start = pos % cap;
   const long long first = n < cap - start ? n : cap - start;
-  for (long long e = threadIdx.x; e < first; e += nthreads) dst[e] = ring[start + e];
-  for (long long e = first + threadIdx.x; e < n; e += nthreads) dst[e] = ring[e - first];
+  copy_span(ring + start, dst, first, nthreads);
+  copy_span(ring, dst + first, n - first, nthreads);
 }
 
 __device__ __forceinline__ long long ring_target(const GaussStreams& G, long long cur,
