@@ -306,6 +306,25 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
   double* T1 = K ? C.buf<double>("T1", (size_t)K * bs * T) : nullptr;
 
   AraOperator op;
+  // H_s (U_k,:^T Omega_s) has a long reduction (K = sum_j rank(k, j), up to
+  // ~4000 at cfg3) over few output tiles (rows x bs = 4 CTA tiles at m = 512):
+  // split it into S chunks of ~512 written to a workspace (beside the U^A
+  // product, which they do not depend on), then Y -= [W_0 .. W_S-1] [I; ..; I]
+  // as one more GEMM (products with exact 1/0, chunks summed in order:
+  // deterministic)
+  const int ksplit = K >= 1024 ? std::min(8, K / 512) : 1;
+  const int kchunk = ksplit > 1 ? ((K + ksplit - 1) / ksplit + 15) / 16 * 16 : K;
+  double* Wsplit = nullptr;
+  double* Istack = nullptr;
+  if (ksplit > 1) {
+    int rmax = 0;
+    for (int s = 0; s < T; ++s) rmax = std::max(rmax, S.rows[s]);
+    Wsplit = C.buf<double>("Ysplit", (size_t)T * ksplit * rmax * bs);
+    std::vector<double> hI((size_t)ksplit * bs * bs, 0.0);
+    for (int c = 0; c < ksplit; ++c)
+      for (int j = 0; j < bs; ++j) hI[(size_t)c * bs + j + (size_t)j * ksplit * bs] = 1.0;
+    Istack = C.push(hI);  // lives in the column's descriptor arena, like the GEMM plans
+  }
   // Y_s = U^A (V^A^T Omega_s) - H_s (U_k,:^T Omega_s)   (Eq. 1 with the j-sum in H)
   op.sample_plan = [&](const double* Om, double* Y, long long Ystride, const int* done,
                        std::vector<std::vector<GemmProblem>>& stages) {
@@ -334,7 +353,26 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
       y.C = Y + s * Ystride; y.ldc = S.rows[s];
       y.M = S.rows[s]; y.N = bs; y.K = kA[s]; y.alpha = 1.0; y.beta = 0.0; y.skip = done + s;
       stages[1].push_back(y);
-      if (K > 0) {
+      if (K > 0 && ksplit > 1) {
+        const int rs = S.rows[s];
+        double* Ws = Wsplit + (size_t)s * ksplit * rs * bs;
+        for (int c = 0; c < ksplit; ++c) {
+          const int k0 = c * kchunk, kc = std::min(K, k0 + kchunk) - k0;
+          GemmProblem h{};
+          h.A = H + s * Hstride + (long long)k0 * rs; h.lda = rs;
+          h.B = T1 + (size_t)s * bs * K + k0; h.ldb = K;
+          h.C = Ws + (size_t)c * rs * bs; h.ldc = rs;
+          h.M = rs; h.N = bs; h.K = std::max(kc, 0); h.alpha = 1.0; h.beta = 0.0;
+          h.skip = done + s;
+          stages[1].push_back(h);
+        }
+        GemmProblem r{};
+        r.A = Ws; r.lda = rs;
+        r.B = Istack; r.ldb = (long long)ksplit * bs;
+        r.C = Y + s * Ystride; r.ldc = rs;
+        r.M = rs; r.N = bs; r.K = ksplit * bs; r.alpha = -1.0; r.beta = 1.0; r.skip = done + s;
+        stages[2].push_back(r);
+      } else if (K > 0) {
         GemmProblem h{};
         h.A = H + s * Hstride; h.lda = S.rows[s];
         h.B = T1 + (size_t)s * bs * K; h.ldb = K;

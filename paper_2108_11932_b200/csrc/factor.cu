@@ -784,11 +784,14 @@ std::unique_ptr<Factor> factorize(Ctx& C, std::unique_ptr<Matrix> A, int mode, c
       TLRG_CUDA(cudaStreamWaitEvent(C.sd, e1.e, 0));
       {
         StreamScope on_diag(C, C.sd);
+        // grow the H_k buffer before the phase timer starts: a growth frees
+        // the old buffer (cudaFree waits for the whole device, i.e. the
+        // column's ARA already in flight) and would land in t_dense
+        double* Hk = cs.K > 0 && !pivoted ? C.buf<double>("Hk", (size_t)b * cs.K) : nullptr;
         cudaEventRecord(de0.e, C.st);
         // keep A_kk: the tile is factored in place and a retry re-reads it
         dcopy(diagk, aorig, (long long)rk * rk, C.st);
         if (cs.K > 0 && !pivoted) {
-          double* Hk = C.buf<double>("Hk", (size_t)b * cs.K);
           std::vector<int> tk{k};
           column_H(C, M, cs, tk, Hk, (long long)b * cs.K);
           std::vector<GemmProblem> pr(1);
