@@ -149,6 +149,30 @@ def test_potrf_matches_reference(tg, ref, n):
     assert fail >= 0
 
 
+def test_chol_ara_update_split_k_sampling(tg, ref):
+    """Graph path (bs = 32, m = 512) at a column whose sampling reduction
+    K = sum_j rank(k, j) exceeds 1024, so the H-product is split into K chunks
+    summed by the stacked-identity GEMM: per tile the same rank, rounds and
+    convergence as the reference, factors within 1e-9 (test_ara.cpp:294-318)."""
+    from helpers import points
+    from paper_2108_11932_b200 import geometry as G
+    n, b, eps, bs, k = 512 * 18, 512, 1e-6, 32, 15
+    A_ref = ref.build(points(G.GRID3D, n, b, 0), 1, 0.2, 1e-4, b, eps, 0, bs, 12345)
+    A = to_gpu(tg, A_ref)
+    rk = A.ranks()
+    K = sum(int(rk[k * (k - 1) // 2 + j]) for j in range(k))
+    assert K >= 1024, K  # the split-K path is taken
+    cfg = tg.AraConfig(block_samples=bs, eps=eps, seed=91)
+    got = tg.chol_ara_update(A, None, k, cfg, tg.AraWorkspace())
+    want = ref.chol_ara_update(A_ref, k, bs=bs, eps=eps, seed=91)
+    assert [t.i for t in got] == [t["i"] for t in want]
+    for g, w in zip(got, want):
+        assert (g.Q.shape[1], g.rounds_resident, g.converged) == \
+            (w["Q"].shape[1], w["rounds"], w["converged"]), g.i
+        d1, d2 = g.Q @ g.B.T, w["Q"] @ w["B"].T
+        assert np.abs(d1 - d2).max() <= 1e-9 * max(np.linalg.norm(d2), 1.0)
+
+
 def _decaying(r, m, n, decades=10.0):
     U, _ = np.linalg.qr(r.normal(size=(m, n)))
     W, _ = np.linalg.qr(r.normal(size=(n, n)))
