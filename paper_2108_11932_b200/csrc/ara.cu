@@ -696,7 +696,6 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
     // narrow tiles' QR + Jacobi run beside them on the side stream
     cudaEvent_t rfork = nullptr, rjoin = nullptr;
     const bool split = !svdw.empty() && !tasks.empty();
-    cudaStream_t st_main = C.st;
     if (split) {
       TLRG_CUDA(cudaEventCreateWithFlags(&rfork, cudaEventDisableTiming));
       TLRG_CUDA(cudaEventCreateWithFlags(&rjoin, cudaEventDisableTiming));
@@ -710,8 +709,9 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
       jacobi_svd_wide(C.push(svdw), (int)svdw.size(), svdw[0].n, C.st, cols);
       ++C.launches;
     }
-    if (split) C.st = C.st2;
     if (!tasks.empty()) {
+      // (on the side stream when split; the scope restores C.st on every exit)
+      StreamScope side(C, split ? C.st2 : C.st);
       PanelTask* d_tasks = C.push(tasks);
       panel_tau(d_tasks, (int)tasks.size(), C.st);
       panel_mgs(d_tasks, (int)tasks.size(), 0, 0, qmax_n, cols, C.st);
@@ -730,7 +730,6 @@ void ara_batch(Ctx& C, const AraSlots& S, const AraOperator& op, const AraCfg& c
         jacobi_svd(d_svd + nwr, (int)svd.size() - nwr, svd[nwr].n, C.st);
     }
     if (split) {
-      C.st = st_main;
       TLRG_CUDA(cudaEventRecord(rjoin, C.st2));
       TLRG_CUDA(cudaStreamWaitEvent(C.st, rjoin, 0));
       cudaEventDestroy(rfork);
