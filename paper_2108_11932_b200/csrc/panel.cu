@@ -242,6 +242,23 @@ struct PanelSmem {
   int buf;
 };
 
+// Lane-strided dot product over the panel rows with four independent partial
+// sums (summed (a0 + a1) + (a2 + a3)): the per-step dot lists are the column
+// sweep's critical path and a single FMA chain serializes on every load.
+__device__ __forceinline__ double panel_dot(const double* __restrict__ a,
+                                            const double* __restrict__ b, int rows, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int r = lane;
+  for (; r + 96 < rows; r += 128) {
+    a0 += a[r] * b[r];
+    a1 += a[r + 32] * b[r + 32];
+    a2 += a[r + 64] * b[r + 64];
+    a3 += a[r + 96] * b[r + 96];
+  }
+  for (; r < rows; r += 32) a0 += a[r] * b[r];
+  return (a0 + a1) + (a2 + a3);
+}
+
 // Block-reduce `nv` per-thread partial values (already warp-summed into lane 0)
 // -> cbuf[0..nv).  One __syncthreads.
 __device__ __forceinline__ void reduce_to(PanelSmem& S, int nv) {
@@ -458,8 +475,7 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
       const int ii = e - jj * (jj + 1) / 2;
       const double* xa = Y + (long long)ii * rows;
       const double* xb = Y + (long long)jj * rows;
-      double sacc = 0.0;
-      for (int r = lane; r < rows; r += 32) sacc += xa[r] * xb[r];
+      double sacc = panel_dot(xa, xb, rows, lane);
       sacc = warp_sum(sacc);
       if (lane == 0) {
         const double f = sacc - (ii == jj ? 1.0 : 0.0);
@@ -523,8 +539,7 @@ __global__ void __launch_bounds__(PT) panel_mgs_kernel(PanelTask* tasks, int swe
         xa = v;
         xb = ys;
       }
-      double sacc = 0.0;
-      for (int r = lane; r < rows; r += 32) sacc += xa[r] * xb[r];
+      double sacc = panel_dot(xa, xb, rows, lane);
       sacc = warp_sum(sacc);
       if (lane == 0) S.cbuf[t] = sacc;
     }
