@@ -102,7 +102,11 @@ static int big_config(const std::vector<GemmProblem>& probs) {
   // leave SMs idle and the 64 x 32 kernel wins
   if (work < (1LL << 24) || minM < 128) return 0;
   if (minN >= 64 && t64 >= 120) return 1;
-  if (maxN <= 32 && minN >= 24 && t32 >= 120) return 2;
+  // the 128 x 32 tiles lost to the 64 x 32 kernel on the bs = 32 round lists once
+  // the long reductions were split (cfg3 3.43 -> 3.22 s, cfg4 14.39 -> 13.60 s,
+  // measured A/B on one box): opt-in only (TLRG_GEMM_BIG32=1)
+  const char* e32 = std::getenv("TLRG_GEMM_BIG32");
+  if (maxN <= 32 && minN >= 24 && t32 >= 120 && e32 && e32[0] == '1') return 2;
   return 0;
 }
 
