@@ -312,7 +312,15 @@ std::vector<TileResult> column_ara(Ctx& C, const Matrix& M, int k, const ColumnS
   // product, which they do not depend on), then Y -= [W_0 .. W_S-1] [I; ..; I]
   // as one more GEMM (products with exact 1/0, chunks summed in order:
   // deterministic)
-  const int ksplit = K >= 1024 ? std::min(8, K / 512) : 1;
+  static const int ks_min = [] {  // TLRG_KSPLIT_MIN / _CHUNK: tuning switches
+    const char* e = std::getenv("TLRG_KSPLIT_MIN");
+    return e ? std::atoi(e) : 1024;
+  }();
+  static const int ks_chunk = [] {
+    const char* e = std::getenv("TLRG_KSPLIT_CHUNK");
+    return e ? std::max(64, std::atoi(e)) : 512;
+  }();
+  const int ksplit = K >= ks_min ? std::max(1, std::min(8, K / ks_chunk)) : 1;
   const int kchunk = ksplit > 1 ? ((K + ksplit - 1) / ksplit + 15) / 16 * 16 : K;
   double* Wsplit = nullptr;
   double* Istack = nullptr;
